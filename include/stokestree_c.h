@@ -1,0 +1,196 @@
+/*
+ * stokestree_c.h -- C ABI of the B200-native treecode (libstokestree_b200.so).
+ *
+ * Drop-in boundary for the reference's public C++ entry points in
+ * /root/reference/proj/include/stokestree/ (header-only C++20 library).  Every
+ * entry point below names the reference interface it replaces (file:line).
+ * The C++ shim (include/stokestree/ headers) re-exposes the reference's exact
+ * names on top of this ABI; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Vec3 arrays are interleaved x,y,z doubles
+ *    (the reference's std::vector<Vec3> storage, vec3.hpp:9-46), n entries.
+ *  - Host pointers unless the function name ends in _device.
+ *  - Every call returns an st_status; on failure st_last_error() (thread-local)
+ *    holds the message the reference would have thrown.
+ *      ST_INVALID_ARGUMENT -> std::invalid_argument
+ *      ST_DOMAIN_ERROR     -> std::domain_error
+ *      ST_CUDA_ERROR / ST_NCCL_ERROR / ST_RUNTIME_ERROR -> std::runtime_error
+ *  - All arithmetic is fp64 on the GPU.  There is no CPU fallback: without a
+ *    usable sm_100 device every compute entry point fails with ST_CUDA_ERROR.
+ */
+#ifndef STOKESTREE_C_H
+#define STOKESTREE_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_ABI_VERSION 1
+
+typedef enum st_status {
+    ST_OK = 0,
+    ST_INVALID_ARGUMENT = 1,
+    ST_DOMAIN_ERROR = 2,
+    ST_CUDA_ERROR = 3,
+    ST_NCCL_ERROR = 4,
+    ST_RUNTIME_ERROR = 5
+} st_status;
+
+/* ParticleSet (particles.hpp:29-36).  dipole_weight/normal may be NULL when
+ * stresslets are off; force_weight may be NULL when Stokeslets are off. */
+typedef struct st_particles {
+    size_t n;
+    const double* position;
+    const double* force_weight;
+    const double* dipole_weight;
+    const double* normal;
+} st_particles;
+
+/* TreecodeParams (engine.hpp:21-42) + KernelSelection (particles.hpp:13-25).
+ * `workers` is validated (>= 1) and otherwise ignored: the GPU path is
+ * bit-identical for every worker count, as the reference promises
+ * (engine.hpp:163-169).  `devices` (new, trailing) is the GPU count (>= 1). */
+typedef struct st_params {
+    int order;          /* p in [0, 16]                      */
+    double theta;       /* MAC parameter, strictly in (0, 1) */
+    int leaf_capacity;  /* N0 >= 1                           */
+    int shrink;         /* bool                              */
+    int stokeslet;      /* bool                              */
+    int stresslet;      /* bool                              */
+    int workers;        /* >= 1, accepted and ignored        */
+    int devices;        /* >= 1                              */
+} st_params;
+
+/* TraversalStats (engine.hpp:44-55) + VelocityResult timings (:57-64).
+ * time_* are device (CUDA-event) seconds of the phases; time_far_s and
+ * time_near_s are the far-field and near-field kernels alone. */
+typedef struct st_stats {
+    uint64_t farfield_evals;
+    uint64_t direct_pairs;
+    uint64_t clusters_visited;
+    double time_build_s;
+    double time_moments_s;
+    double time_traverse_s;
+    double time_total_s;
+    double time_far_s;
+    double time_near_s;
+    double time_h2d_s;
+    double time_d2h_s;
+    uint64_t gpu_launches; /* kernels this call launched */
+} st_stats;
+
+typedef struct st_tree st_tree;
+
+int st_abi_version(void);
+const char* st_last_error(void);
+/* Number of visible CUDA devices (0 when none / no driver). */
+st_status st_device_count(int* out);
+
+/* ---- validation (pure host, no GPU needed) ---- */
+/* TreecodeParams::validate (engine.hpp:31-41). */
+st_status st_params_validate(const st_params* params);
+
+/* ---- the treecode path ---- */
+/* treecode_velocity / parallel_velocity (engine.hpp:185-196, run_treecode :133-180):
+ * validate (engine.hpp:31-41, particles.hpp:41-70), build the tree, compute the
+ * moments, traverse every target; u_out[3n] in ORIGINAL particle order. */
+st_status st_treecode_velocity(const st_particles* src, const st_params* params, double* u_out,
+                               st_stats* stats);
+
+/* Extended form.  targets == NULL: targets are the sources (self excluded by
+ * tree index, engine.hpp:118-131).  Otherwise n_targets disjoint points
+ * (xyz interleaved), nothing excluded (skip = kNoSkip, kernels.hpp:43) -- the
+ * entry cfg4 needs, absent from the reference's public API.
+ * per_target (optional, 3 * n_targets uint64, ORIGINAL target order):
+ * {clusters_visited, farfield_evals, direct_pairs} of each target. */
+st_status st_treecode_velocity_ex(const st_particles* src, const double* targets, size_t n_targets,
+                                  const st_params* params, double* u_out, uint64_t* per_target,
+                                  st_stats* stats);
+
+/* Device-resident form: every pointer (src arrays, targets, u_out) is device
+ * memory on the current device; work is issued on `stream` (cudaStream_t,
+ * NULL = the legacy default stream).  shard / n_shards select a contiguous,
+ * work-balanced range of the Morton-ordered target batches (n_shards = 1:
+ * all); only that shard's entries of u_out are written.  This is the entry a
+ * multi-process (one rank per GPU) driver uses; the tree and moments are
+ * rebuilt redundantly and bit-identically on every rank. */
+st_status st_treecode_velocity_device(const st_particles* src_device, const double* targets_device,
+                                      size_t n_targets, const st_params* params,
+                                      double* u_out_device, int shard, int n_shards,
+                                      void* stream, st_stats* stats);
+
+/* ---- direct sums (O(N^2) oracle path) ---- */
+/* contracted_direct_velocity(ps, sel, first, last) (kernels.hpp:123-136). */
+st_status st_direct_velocity(const st_particles* src, int stokeslet, int stresslet, size_t first,
+                             size_t last, double* u_out);
+/* contracted_direct_velocity_at (kernels.hpp:139-150). */
+st_status st_direct_velocity_at(const st_particles* src, int stokeslet, int stresslet,
+                                const size_t* targets, size_t n_targets, double* u_out);
+/* naive_direct_velocity (kernels.hpp:89-118): forms S_ij and T_ijl per pair. */
+st_status st_naive_direct_velocity(const st_particles* src, int stokeslet, int stresslet,
+                                   double* u_out);
+
+/* ---- tree and moments ---- */
+/* build_tree (cluster_tree.hpp:152-192).  Clusters in pre-order (id 0 = root). */
+st_status st_build_tree(const st_particles* src, int leaf_capacity, int shrink, st_tree** out);
+size_t st_tree_num_clusters(const st_tree* tree);
+size_t st_tree_num_particles(const st_tree* tree);
+/* Export (any pointer may be NULL):
+ *   begin_end[2*ncl] (Cluster::begin/end), geom[10*ncl] = center xyz, radius,
+ *   bbox lo xyz, bbox hi xyz; children[8*ncl] (-1 padded, slot order);
+ *   meta[2*ncl] = n_children, is_leaf; to_original[n] (ClusterTree::to_original). */
+st_status st_tree_export(const st_tree* tree, int64_t* begin_end, double* geom, int32_t* children,
+                         int32_t* meta, uint32_t* to_original);
+void st_tree_free(st_tree* tree);
+
+/* compute_moments (moments.hpp:140-175) in the reference layout (:15-27):
+ * stok[ncl*E*3], str[ncl*E*9], trace[ncl*E], sym[ncl*E*6], E = (p+1)(p+2)(p+3)/6.
+ * Buffers of a disabled kernel may be NULL. */
+st_status st_compute_moments(const st_tree* tree, int order, int stokeslet, int stresslet,
+                             double* stok, double* str, double* trace, double* sym);
+
+/* ---- per-pair far-field API, batched (coulomb.hpp:28-59, farfield.hpp:30-96) ---- */
+/* b^k for every k with |k| <= pmax, graded-lex order (multi_index.hpp:36-44), at
+ * n_pairs displacements dx[3*n_pairs]; b_out[n_pairs * E(pmax)]. */
+st_status st_coulomb_coeffs(size_t n_pairs, const double* dx, int pmax, double* b_out);
+/* stokeslet_farfield + stresslet_farfield for n_pairs (dx, moment block) pairs; moment
+ * blocks in the reference layout, one block of E(p) entries per pair. */
+st_status st_farfield_pairs(size_t n_pairs, const double* dx, int order, int stokeslet,
+                            int stresslet, const double* stok, const double* str,
+                            const double* trace, const double* sym, double* u_out);
+
+/* ---- metric (error_metric.hpp:13-24), host ---- */
+st_status st_relative_error(size_t n, const double* u_ref, const double* u_test, double* out);
+
+/* ---- multi-GPU planning (host, no GPU needed) ---- */
+/* Contiguous work-balanced cut points: given per-unit weights w[n_units] (any
+ * non-negative cost), write cuts[n_shards+1] with cuts[0] = 0, cuts[n_shards] =
+ * n_units, such that shard s owns [cuts[s], cuts[s+1]) and the prefix-weight
+ * boundaries are as close as possible to s/n_shards of the total. */
+st_status st_shard_cuts(size_t n_units, const double* weights, int n_shards, size_t* cuts);
+
+/* ---- seeded synthetic inputs (host) ---- */
+enum {
+    ST_GEN_UNIT = 0,    /* testutil::random_particles: positions in [0,1)^3       */
+    ST_GEN_CUBE = 1,    /* BASELINE cfg0/1/3: positions in [-0.5,0.5)^3            */
+    ST_GEN_SPHERE = 2,  /* cfg2: uniform on the unit sphere, nu = outward normal   */
+    ST_GEN_MIXTURE = 3, /* cfg4 sources: 16 Gaussians, sigma 0.05                 */
+    ST_GEN_POINTS = 4   /* cfg4 targets: positions only, [-0.5,0.5)^3              */
+};
+st_status st_generate(int kind, size_t n, uint64_t seed, int with_stresslets, double* pos,
+                      double* f, double* h, double* nu);
+
+/* ---- measurement ---- */
+/* FP64 FMA throughput probe (a DFMA-only kernel over every SM): TFLOP/s with
+ * FMA = 2 flop, run for roughly `seconds`. */
+st_status st_fp64_peak(double seconds, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STOKESTREE_C_H */

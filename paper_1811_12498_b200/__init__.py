@@ -1,0 +1,514 @@
+"""B200-native Stokeslet/stresslet treecode (arXiv 1811.12498 hot path).
+
+Python mirror of the reference's public C++ API (namespace ``stokestree`` in
+/root/reference/proj/include/stokestree/*.hpp) over the C ABI of
+``libstokestree_b200.so`` (include/stokestree_c.h).  Names, argument meaning
+and error behaviour follow the reference:
+
+=========================================  ==========================================
+reference (file:line)                      here
+=========================================  ==========================================
+KernelSelection (particles.hpp:13-25)       KernelSelection
+ParticleSet / validate (particles.hpp:29-70) ParticleSet (arrays are (n, 3) float64)
+TreecodeParams (engine.hpp:21-42)           TreecodeParams (+ ``devices``)
+TraversalStats, VelocityResult (:44-64)     TraversalStats, VelocityResult
+treecode_velocity (engine.hpp:185-189)      treecode_velocity
+parallel_velocity (engine.hpp:194-196)      parallel_velocity
+contracted_direct_velocity (kernels.hpp)    contracted_direct_velocity(_at)
+naive_direct_velocity (kernels.hpp:89-118)  naive_direct_velocity
+build_tree (cluster_tree.hpp:152-192)       build_tree -> ClusterTree
+compute_moments (moments.hpp:140-175)       compute_moments -> ClusterMoments
+coulomb_coeffs (coulomb.hpp:52-59)          coulomb_coeffs (batched)
+stokeslet/stresslet_farfield (farfield.hpp) farfield_pairs (batched)
+relative_error (error_metric.hpp:13-24)     relative_error
+=========================================  ==========================================
+
+std::invalid_argument -> :class:`InvalidArgument` (a ValueError),
+std::domain_error -> :class:`DomainError` (an ArithmeticError), CUDA/runtime
+failures -> :class:`StokesTreeError` (a RuntimeError).  There is no CPU
+fallback: every compute call runs the sm_100a kernels and fails loudly without
+a device or without the built library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "KernelSelection", "ParticleSet", "TreecodeParams", "TraversalStats", "VelocityResult",
+    "ClusterTree", "ClusterMoments", "InvalidArgument", "DomainError", "StokesTreeError",
+    "treecode_velocity", "parallel_velocity", "treecode_velocity_targets",
+    "treecode_velocity_device", "contracted_direct_velocity", "contracted_direct_velocity_at",
+    "naive_direct_velocity", "build_tree", "compute_moments", "coulomb_coeffs",
+    "farfield_pairs", "relative_error", "generate", "shard_cuts", "fp64_peak", "device_count",
+    "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libstokestree_b200.so")
+
+# every symbol declared in include/stokestree_c.h
+EXPORTED_SYMBOLS = (
+    "st_abi_version", "st_last_error", "st_device_count", "st_params_validate",
+    "st_treecode_velocity", "st_treecode_velocity_ex", "st_treecode_velocity_device",
+    "st_direct_velocity", "st_direct_velocity_at", "st_naive_direct_velocity", "st_build_tree",
+    "st_tree_num_clusters", "st_tree_num_particles", "st_tree_export", "st_tree_free",
+    "st_compute_moments", "st_coulomb_coeffs", "st_farfield_pairs", "st_relative_error",
+    "st_shard_cuts", "st_generate", "st_fp64_peak",
+)
+
+GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
+_GEN = {"unit": GEN_UNIT, "cube": GEN_CUBE, "sphere": GEN_SPHERE, "mixture": GEN_MIXTURE,
+        "points": GEN_POINTS}
+
+
+class StokesTreeError(RuntimeError):
+    """CUDA / NCCL / runtime failure (std::runtime_error in the reference)."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument."""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error (coincident points, zero displacement, zero reference field)."""
+
+
+# ------------------------------------------------------------------ C structs
+class _Particles(C.Structure):
+    _fields_ = [("n", C.c_size_t), ("position", C.c_void_p), ("force_weight", C.c_void_p),
+                ("dipole_weight", C.c_void_p), ("normal", C.c_void_p)]
+
+
+class _Params(C.Structure):
+    _fields_ = [("order", C.c_int), ("theta", C.c_double), ("leaf_capacity", C.c_int),
+                ("shrink", C.c_int), ("stokeslet", C.c_int), ("stresslet", C.c_int),
+                ("workers", C.c_int), ("devices", C.c_int)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("farfield_evals", C.c_uint64), ("direct_pairs", C.c_uint64),
+                ("clusters_visited", C.c_uint64), ("time_build_s", C.c_double),
+                ("time_moments_s", C.c_double), ("time_traverse_s", C.c_double),
+                ("time_total_s", C.c_double), ("time_far_s", C.c_double),
+                ("time_near_s", C.c_double), ("time_h2d_s", C.c_double),
+                ("time_d2h_s", C.c_double), ("gpu_launches", C.c_uint64)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load the in-tree CUDA library; raise loudly when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise StokesTreeError(
+            f"CUDA library {lib_path} is missing: build it with `make -C paper_1811_12498_b200` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    L = C.CDLL(lib_path)
+    vp, sz, i, d = C.c_void_p, C.c_size_t, C.c_int, C.c_double
+    P = C.POINTER
+    L.st_abi_version.restype = i
+    L.st_last_error.restype = C.c_char_p
+    L.st_device_count.argtypes = [P(i)]
+    L.st_params_validate.argtypes = [P(_Params)]
+    L.st_treecode_velocity.argtypes = [P(_Particles), P(_Params), vp, P(_Stats)]
+    L.st_treecode_velocity_ex.argtypes = [P(_Particles), vp, sz, P(_Params), vp, vp, P(_Stats)]
+    L.st_treecode_velocity_device.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, i, vp, P(_Stats)]
+    L.st_direct_velocity.argtypes = [P(_Particles), i, i, sz, sz, vp]
+    L.st_direct_velocity_at.argtypes = [P(_Particles), i, i, vp, sz, vp]
+    L.st_naive_direct_velocity.argtypes = [P(_Particles), i, i, vp]
+    L.st_build_tree.argtypes = [P(_Particles), i, i, P(vp)]
+    L.st_tree_num_clusters.restype = sz
+    L.st_tree_num_clusters.argtypes = [vp]
+    L.st_tree_num_particles.restype = sz
+    L.st_tree_num_particles.argtypes = [vp]
+    L.st_tree_export.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.st_tree_free.argtypes = [vp]
+    L.st_tree_free.restype = None
+    L.st_compute_moments.argtypes = [vp, i, i, i, vp, vp, vp, vp]
+    L.st_coulomb_coeffs.argtypes = [sz, vp, i, vp]
+    L.st_farfield_pairs.argtypes = [sz, vp, i, i, i, vp, vp, vp, vp, vp]
+    L.st_relative_error.argtypes = [sz, vp, vp, P(d)]
+    L.st_shard_cuts.argtypes = [sz, vp, i, vp]
+    L.st_generate.argtypes = [i, sz, C.c_uint64, i, vp, vp, vp, vp]
+    L.st_fp64_peak.argtypes = [d, P(d)]
+    for name in EXPORTED_SYMBOLS:
+        if name not in ("st_abi_version", "st_last_error", "st_tree_num_clusters",
+                        "st_tree_num_particles", "st_tree_free"):
+            getattr(L, name).restype = i
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code == 0:
+        return
+    msg = load_library().st_last_error().decode()
+    if code == 1:
+        raise InvalidArgument(msg)
+    if code == 2:
+        raise DomainError(msg)
+    raise StokesTreeError(msg)
+
+
+def mi_count(p: int) -> int:
+    """Entries with |k| <= p (multi_index.hpp:19-20)."""
+    return (p + 1) * (p + 2) * (p + 3) // 6
+
+
+# ------------------------------------------------------------------ data model
+@dataclass(frozen=True)
+class KernelSelection:
+    stokeslet_enabled: bool = True
+    stresslet_enabled: bool = True
+
+    @staticmethod
+    def stokeslet_only():
+        return KernelSelection(True, False)
+
+    @staticmethod
+    def stresslet_only():
+        return KernelSelection(False, True)
+
+    @staticmethod
+    def both():
+        return KernelSelection(True, True)
+
+
+def _as3(a):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size == 0:
+        return None
+    return a.reshape(-1, 3)
+
+
+@dataclass
+class ParticleSet:
+    """Structure of arrays, (n, 3) float64 each; h / nu may be None without stresslets."""
+    position: np.ndarray
+    force_weight: Optional[np.ndarray] = None
+    dipole_weight: Optional[np.ndarray] = None
+    normal: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        self.position = _as3(self.position)
+        if self.position is None:
+            self.position = np.zeros((0, 3))
+        self.force_weight = _as3(self.force_weight)
+        self.dipole_weight = _as3(self.dipole_weight)
+        self.normal = _as3(self.normal)
+
+    def size(self) -> int:
+        return len(self.position)
+
+    def _c(self, sel: Optional[KernelSelection] = None) -> _Particles:
+        n = len(self.position)
+
+        def ptr(a, needed=True):
+            if a is None or not needed:
+                return None
+            if len(a) != n:  # mismatched length: hand the library a NULL array
+                return None
+            return a.ctypes.data
+
+        sto = True if sel is None else sel.stokeslet_enabled
+        stre = True if sel is None else sel.stresslet_enabled
+        return _Particles(n, ptr(self.position), ptr(self.force_weight, sto),
+                          ptr(self.dipole_weight, stre), ptr(self.normal, stre))
+
+
+@dataclass
+class TreecodeParams:
+    kMaxOrder = 16
+    order: int = 6
+    theta: float = 0.5
+    leaf_capacity: int = 2000
+    shrink: bool = True
+    kernels: KernelSelection = field(default_factory=KernelSelection)
+    workers: int = 1
+    devices: int = 1
+
+    def _c(self) -> _Params:
+        return _Params(int(self.order), float(self.theta), int(self.leaf_capacity), int(bool(self.shrink)),
+                       int(self.kernels.stokeslet_enabled), int(self.kernels.stresslet_enabled),
+                       int(self.workers), int(self.devices))
+
+    def validate(self):
+        """TreecodeParams::validate (engine.hpp:31-41)."""
+        p = self._c()
+        _check(load_library().st_params_validate(C.byref(p)))
+
+
+@dataclass
+class TraversalStats:
+    farfield_evals: int = 0
+    direct_pairs: int = 0
+    clusters_visited: int = 0
+
+
+@dataclass
+class VelocityResult:
+    velocity: np.ndarray
+    stats: TraversalStats
+    time_build_s: float = 0.0
+    time_moments_s: float = 0.0
+    time_traverse_s: float = 0.0
+    time_total_s: float = 0.0
+    time_far_s: float = 0.0
+    time_near_s: float = 0.0
+    time_h2d_s: float = 0.0
+    time_d2h_s: float = 0.0
+    gpu_launches: int = 0
+    per_target: Optional[np.ndarray] = None
+
+
+def _result(u, s: _Stats, per_target=None) -> VelocityResult:
+    return VelocityResult(u, TraversalStats(int(s.farfield_evals), int(s.direct_pairs), int(s.clusters_visited)),
+                          s.time_build_s, s.time_moments_s, s.time_traverse_s, s.time_total_s, s.time_far_s,
+                          s.time_near_s, s.time_h2d_s, s.time_d2h_s, int(s.gpu_launches), per_target)
+
+
+# ------------------------------------------------------------------ the treecode
+def treecode_velocity_targets(ps: ParticleSet, targets, params: TreecodeParams,
+                              per_target: bool = False) -> VelocityResult:
+    """Treecode at explicit targets (None: the sources themselves, self excluded)."""
+    L = load_library()
+    cp = ps._c(params.kernels)
+    prm = params._c()
+    tg = _as3(targets) if targets is not None else None
+    if targets is not None and tg is None:
+        raise InvalidArgument("targets: empty target set")
+    nt = ps.size() if tg is None else len(tg)
+    u = np.zeros((nt, 3))
+    pt = np.zeros((nt, 3), np.uint64) if per_target else None
+    st = _Stats()
+    _check(L.st_treecode_velocity_ex(C.byref(cp), None if tg is None else tg.ctypes.data,
+                                     0 if tg is None else len(tg), C.byref(prm), u.ctypes.data,
+                                     None if pt is None else pt.ctypes.data, C.byref(st)))
+    return _result(u, st, pt)
+
+
+def treecode_velocity(ps: ParticleSet, params: TreecodeParams, per_target: bool = False) -> VelocityResult:
+    """Single-worker treecode (engine.hpp:185-189); velocities in original order."""
+    return treecode_velocity_targets(ps, None, params, per_target)
+
+
+def parallel_velocity(ps: ParticleSet, params: TreecodeParams, per_target: bool = False) -> VelocityResult:
+    """Replicated-data driver (engine.hpp:194-196); bit-identical to treecode_velocity."""
+    return treecode_velocity_targets(ps, None, params, per_target)
+
+
+def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],
+                             normal_ptr: Optional[int], n: int, params: TreecodeParams, u_out_ptr: int,
+                             targets_ptr: Optional[int] = None, n_targets: int = 0, shard: int = 0,
+                             n_shards: int = 1, stream: int = 0) -> VelocityResult:
+    """Device-resident call: raw device pointers (e.g. torch ``data_ptr()``) and a CUDA stream."""
+    L = load_library()
+    cp = _Particles(n, position_ptr, force_ptr, dipole_ptr, normal_ptr)
+    prm = params._c()
+    st = _Stats()
+    _check(L.st_treecode_velocity_device(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr,
+                                         shard, n_shards, stream, C.byref(st)))
+    return _result(None, st)
+
+
+# ------------------------------------------------------------------ direct sums
+def contracted_direct_velocity(ps: ParticleSet, sel: KernelSelection, first: int = 0,
+                               last: Optional[int] = None) -> np.ndarray:
+    """contracted_direct_velocity (kernels.hpp:123-136)."""
+    L = load_library()
+    last = ps.size() if last is None else last
+    if first < 0 or last < 0:
+        raise InvalidArgument("contracted_direct_velocity: bad target range")
+    cp = ps._c(sel)
+    u = np.zeros((max(last - first, 0), 3))
+    _check(L.st_direct_velocity(C.byref(cp), int(sel.stokeslet_enabled), int(sel.stresslet_enabled), first,
+                                last, u.ctypes.data))
+    return u
+
+
+def contracted_direct_velocity_at(ps: ParticleSet, sel: KernelSelection, targets) -> np.ndarray:
+    """contracted_direct_velocity_at (kernels.hpp:139-150)."""
+    L = load_library()
+    tg = np.ascontiguousarray(targets, dtype=np.int64)
+    if (tg < 0).any():
+        raise InvalidArgument("contracted_direct_velocity_at: target out of range")
+    tg = tg.astype(np.uint64)
+    cp = ps._c(sel)
+    u = np.zeros((len(tg), 3))
+    _check(L.st_direct_velocity_at(C.byref(cp), int(sel.stokeslet_enabled), int(sel.stresslet_enabled),
+                                   tg.ctypes.data, len(tg), u.ctypes.data))
+    return u
+
+
+def naive_direct_velocity(ps: ParticleSet, sel: KernelSelection) -> np.ndarray:
+    """naive_direct_velocity (kernels.hpp:89-118): tensor-forming O(N^2) sum."""
+    L = load_library()
+    cp = ps._c(sel)
+    u = np.zeros((ps.size(), 3))
+    _check(L.st_naive_direct_velocity(C.byref(cp), int(sel.stokeslet_enabled), int(sel.stresslet_enabled),
+                                      u.ctypes.data))
+    return u
+
+
+# ------------------------------------------------------------------ tree + moments
+class ClusterTree:
+    """build_tree output (cluster_tree.hpp:34-43), exported to host arrays, pre-order."""
+
+    def __init__(self, handle, n, leaf_capacity, shrink, particles: ParticleSet):
+        L = load_library()
+        self._h = handle
+        self.leaf_capacity = leaf_capacity
+        self.shrink = shrink
+        ncl = L.st_tree_num_clusters(handle)
+        be = np.zeros((ncl, 2), np.int64)
+        geom = np.zeros((ncl, 10))
+        kids = np.zeros((ncl, 8), np.int32)
+        meta = np.zeros((ncl, 2), np.int32)
+        perm = np.zeros(n, np.uint32)
+        _check(L.st_tree_export(handle, be.ctypes.data, geom.ctypes.data, kids.ctypes.data, meta.ctypes.data,
+                                perm.ctypes.data))
+        self.ncl = ncl
+        self.begin, self.end = be[:, 0], be[:, 1]
+        self.geom = geom
+        self.center, self.radius = geom[:, 0:3], geom[:, 3]
+        self.lo, self.hi = geom[:, 4:7], geom[:, 7:10]
+        self.children, self.n_children, self.is_leaf = kids, meta[:, 0], meta[:, 1]
+        self.to_original = perm
+        self.to_tree = np.empty_like(perm)
+        self.to_tree[perm] = np.arange(n, dtype=np.uint32)
+        src = particles
+        self.particles = ParticleSet(src.position[perm],
+                                     None if src.force_weight is None else src.force_weight[perm],
+                                     None if src.dipole_weight is None else src.dipole_weight[perm],
+                                     None if src.normal is None else src.normal[perm])
+
+    @property
+    def clusters(self):
+        return range(self.ncl)
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None:
+            _lib.st_tree_free(h)
+
+
+def build_tree(ps: ParticleSet, leaf_capacity: int, shrink: bool) -> ClusterTree:
+    """build_tree (cluster_tree.hpp:152-192), on the device."""
+    L = load_library()
+    cp = ps._c(None)
+    h = C.c_void_p()
+    _check(L.st_build_tree(C.byref(cp), int(leaf_capacity), int(bool(shrink)), C.byref(h)))
+    return ClusterTree(h.value, ps.size(), leaf_capacity, shrink, ps)
+
+
+@dataclass
+class ClusterMoments:
+    """ClusterMoments (moments.hpp:85-134): [ncl, E, {3, 9, 1, 6}] arrays."""
+    order: int
+    stok: Optional[np.ndarray]
+    str: Optional[np.ndarray]
+    trace: Optional[np.ndarray]
+    sym: Optional[np.ndarray]
+
+    def entry_count(self) -> int:
+        return mi_count(self.order)
+
+
+def compute_moments(tree: ClusterTree, p: int, sel: KernelSelection) -> ClusterMoments:
+    """compute_moments (moments.hpp:140-175), on the device."""
+    L = load_library()
+    E = mi_count(max(p, 0))
+    ncl = tree.ncl
+    sto, stre = sel.stokeslet_enabled, sel.stresslet_enabled
+    a = np.zeros((ncl, E, 3)) if sto else None
+    b = np.zeros((ncl, E, 9)) if stre else None
+    c = np.zeros((ncl, E, 1)) if stre else None
+    d = np.zeros((ncl, E, 6)) if stre else None
+    ptr = lambda x: None if x is None else x.ctypes.data
+    _check(L.st_compute_moments(tree._h, int(p), int(sto), int(stre), ptr(a), ptr(b), ptr(c), ptr(d)))
+    return ClusterMoments(p, a, b, c, d)
+
+
+def coulomb_coeffs(dx, pmax: int) -> np.ndarray:
+    """b^k for |k| <= pmax at each displacement (coulomb.hpp:28-59), graded-lex order."""
+    L = load_library()
+    d = np.ascontiguousarray(dx, np.float64).reshape(-1, 3)
+    b = np.zeros((len(d), mi_count(max(pmax, 0))))
+    _check(L.st_coulomb_coeffs(len(d), d.ctypes.data, int(pmax), b.ctypes.data))
+    return b
+
+
+def farfield_pairs(dx, p: int, stok=None, strm=None, trace=None, sym=None) -> np.ndarray:
+    """stokeslet_farfield + stresslet_farfield (farfield.hpp:30-96) for batches of pairs.
+
+    ``stok`` [n, E, 3] and ``strm`` [n, E, 9] are per-pair moment blocks in the
+    reference layout; pass None to disable a kernel."""
+    L = load_library()
+    d = np.ascontiguousarray(dx, np.float64).reshape(-1, 3)
+    a = None if stok is None else np.ascontiguousarray(stok, np.float64)
+    b = None if strm is None else np.ascontiguousarray(strm, np.float64)
+    u = np.zeros((len(d), 3))
+    ptr = lambda x: None if x is None else x.ctypes.data
+    _check(L.st_farfield_pairs(len(d), d.ctypes.data, int(p), int(a is not None), int(b is not None), ptr(a),
+                               ptr(b), None, None, u.ctypes.data))
+    return u
+
+
+def relative_error(u_ref, u_test) -> float:
+    """E = sqrt(sum |u_ref - u|^2 / sum |u_ref|^2) (error_metric.hpp:13-24)."""
+    a = np.ascontiguousarray(u_ref, np.float64).reshape(-1)
+    b = np.ascontiguousarray(u_test, np.float64).reshape(-1)
+    if a.size != b.size:
+        raise InvalidArgument("relative_error: field lengths differ")
+    out = C.c_double(0)
+    _check(load_library().st_relative_error(a.size // 3, a.ctypes.data, b.ctypes.data, C.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------------ inputs / planning
+def generate(kind: str, n: int, seed: int, with_stresslets: bool = True) -> ParticleSet:
+    """Seeded synthetic inputs: unit | cube | sphere | mixture | points."""
+    L = load_library()
+    k = _GEN[kind]
+    pos = np.zeros((n, 3))
+    if k == GEN_POINTS:
+        _check(L.st_generate(k, n, seed, 0, pos.ctypes.data, None, None, None))
+        return ParticleSet(pos)
+    f = np.zeros((n, 3))
+    h = np.zeros((n, 3)) if with_stresslets else None
+    nu = np.zeros((n, 3)) if with_stresslets else None
+    ptr = lambda x: None if x is None else x.ctypes.data
+    _check(L.st_generate(k, n, seed, int(with_stresslets), pos.ctypes.data, f.ctypes.data, ptr(h), ptr(nu)))
+    return ParticleSet(pos, f, h, nu)
+
+
+def shard_cuts(weights, n_shards: int) -> np.ndarray:
+    """Contiguous work-balanced shard boundaries over per-unit weights."""
+    w = np.ascontiguousarray(weights, np.float64)
+    cuts = np.zeros(n_shards + 1, np.uint64)
+    _check(load_library().st_shard_cuts(len(w), w.ctypes.data if len(w) else None, int(n_shards),
+                                        cuts.ctypes.data))
+    return cuts.astype(np.int64)
+
+
+def fp64_peak(seconds: float = 0.2) -> float:
+    """Measured FP64 FMA throughput of the current device, TFLOP/s (FMA = 2 flop)."""
+    out = C.c_double(0)
+    _check(load_library().st_fp64_peak(float(seconds), C.byref(out)))
+    return out.value
+
+
+def device_count() -> int:
+    out = C.c_int(0)
+    load_library().st_device_count(C.byref(out))
+    return out.value

@@ -1,0 +1,758 @@
+// C ABI of libstokestree_b200.so (include/stokestree_c.h): validation with the
+// reference's error taxonomy and messages, device buffer management, and the
+// orchestration of K1 (tree) -> K2 (moments + fold) -> K3/K4 (far) -> K5 (near).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "moments.cuh"
+#include "traverse.cuh"
+#include "tree.cuh"
+
+namespace st {
+thread_local uint64_t g_launches = 0;
+}
+
+using namespace st;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+st_status set_error(st_status s, const std::string& m) {
+    g_last_error = m;
+    return s;
+}
+
+template <class F>
+st_status guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return ST_OK;
+    } catch (const Error& e) {
+        return set_error(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return set_error(ST_RUNTIME_ERROR, "out of host memory");
+    } catch (const std::exception& e) {
+        return set_error(ST_RUNTIME_ERROR, e.what());
+    }
+}
+
+// ------------------------------------------------------------ device context
+std::once_flag g_pool_once[64];
+
+void ensure_device() {
+    int ndev = 0;
+    const cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        fail(ST_CUDA_ERROR, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                "); the treecode has no CPU fallback");
+    int dev = 0;
+    ST_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    ST_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        fail(ST_CUDA_ERROR, "device " + std::to_string(dev) + " is sm_" + std::to_string(prop.major) +
+                                std::to_string(prop.minor) + "; this library is built for sm_100a");
+    if (dev < 64)
+        std::call_once(g_pool_once[dev], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        });
+}
+
+struct OwnedStream {
+    cudaStream_t s = nullptr;
+    OwnedStream() { ST_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~OwnedStream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { ST_CUDA(cudaEventCreate(&e)); }
+    ~Event() {
+        if (e) cudaEventDestroy(e);
+    }
+    void record(cudaStream_t s) { ST_CUDA(cudaEventRecord(e, s)); }
+};
+double secs(const Event& a, const Event& b) {
+    float ms = 0.f;
+    ST_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
+    return ms * 1e-3;
+}
+
+inline unsigned nblocks(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------ small kernels
+// 12-double source record [y, f, h, nu] gathered by `perm` (identity if null).
+__global__ void k_pack(size_t n, const uint32_t* __restrict__ perm, const double* __restrict__ pos,
+                       const double* __restrict__ f, const double* __restrict__ h,
+                       const double* __restrict__ nu, double* __restrict__ rec,
+                       uint32_t* __restrict__ to_tree) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const size_t o = perm ? perm[t] : t;
+    double* r = rec + 12 * t;
+    for (int a = 0; a < 3; ++a) {
+        r[a] = pos[3 * o + a];
+        r[3 + a] = f ? f[3 * o + a] : 0.0;
+        r[6 + a] = h ? h[3 * o + a] : 0.0;
+        r[9 + a] = nu ? nu[3 * o + a] : 0.0;
+    }
+    if (to_tree) to_tree[o] = (uint32_t)t;
+}
+
+// Targets in batch order: positions, original index, excluded source tree index.
+__global__ void k_targets(size_t nt, const uint32_t* __restrict__ tperm, const double* __restrict__ tpos,
+                          const uint32_t* __restrict__ to_tree, double* __restrict__ tx,
+                          uint32_t* __restrict__ torig, uint32_t* __restrict__ tskip) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const uint32_t o = tperm[t];
+    for (int a = 0; a < 3; ++a) tx[3 * t + a] = tpos[3 * (size_t)o + a];
+    torig[t] = o;
+    tskip[t] = to_tree ? to_tree[o] : kNoSkip;
+}
+
+// validate(ps, sel) (particles.hpp:41-70) on device: first failing index per check
+// {position finite, f finite, h finite, nu finite, nu unit (+-1e-12)}.
+__global__ void k_validate(size_t n, const double* __restrict__ pos, const double* __restrict__ f,
+                           const double* __restrict__ h, const double* __restrict__ nu, int str,
+                           unsigned long long* __restrict__ first_bad) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto fin3 = [](const double* a) { return isfinite(a[0]) && isfinite(a[1]) && isfinite(a[2]); };
+    if (!fin3(pos + 3 * i)) atomicMin(&first_bad[0], (unsigned long long)i);
+    if (f && !fin3(f + 3 * i)) atomicMin(&first_bad[1], (unsigned long long)i);
+    if (h && !fin3(h + 3 * i)) atomicMin(&first_bad[2], (unsigned long long)i);
+    if (nu) {
+        const double* v = nu + 3 * i;
+        if (!fin3(v)) atomicMin(&first_bad[3], (unsigned long long)i);
+        if (str) {
+            const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(v[0], v[0]), __dmul_rn(v[1], v[1])),
+                                        __dmul_rn(v[2], v[2]));
+            const double len = __dsqrt_rn(n2);
+            if (fabs(__dsub_rn(len, 1.0)) > 1e-12) atomicMin(&first_bad[4], (unsigned long long)i);
+        }
+    }
+}
+
+__global__ void k_fp64_peak(double* out, int iters, double seed) {
+    double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+           a6 = a0 + 6, a7 = a0 + 7;
+    const double m = 0.999999999, c = 1e-9;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+            a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+        }
+    }
+    const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 12345.678) out[0] = r;  // practically never; keeps the chains live
+}
+
+// ------------------------------------------------------------ validation (host side)
+void validate_params(const st_params* p) {
+    if (!p) fail(ST_INVALID_ARGUMENT, "params: null");
+    if (p->order < 0 || p->order > 16) fail(ST_INVALID_ARGUMENT, "params: order must be in [0, 16]");
+    if (!(p->theta > 0.0) || !(p->theta < 1.0))
+        fail(ST_INVALID_ARGUMENT, "params: theta must lie strictly in (0,1)");
+    if (p->leaf_capacity < 1) fail(ST_INVALID_ARGUMENT, "params: leaf capacity must be >= 1");
+    if (p->workers < 1) fail(ST_INVALID_ARGUMENT, "params: workers must be >= 1");
+    if (!p->stokeslet && !p->stresslet)
+        fail(ST_INVALID_ARGUMENT, "params: at least one kernel must be enabled");
+    if (p->devices < 1) fail(ST_INVALID_ARGUMENT, "params: devices must be >= 1");
+}
+
+// Host-visible part of validate(ps, sel): selection, emptiness, presence ("length").
+void validate_shape(const st_particles* ps, bool sto, bool str) {
+    if (!sto && !str) fail(ST_INVALID_ARGUMENT, "kernel selection: at least one kernel must be enabled");
+    if (!ps || ps->n == 0) fail(ST_INVALID_ARGUMENT, "particle set is empty");
+    auto need = [](const double* a, const char* name) {
+        if (!a)
+            fail(ST_INVALID_ARGUMENT, std::string("particle array '") + name + "' has mismatched length");
+    };
+    need(ps->position, "position");
+    if (sto) need(ps->force_weight, "force_weight");
+    if (str) {
+        need(ps->dipole_weight, "dipole_weight");
+        need(ps->normal, "normal");
+    }
+}
+
+// Device part of validate(ps, sel) on device-resident arrays.
+void validate_values_device(size_t n, const double* pos, const double* f, const double* h, const double* nu,
+                            bool sto, bool str, cudaStream_t s) {
+    DevArray<unsigned long long> bad(5, s);
+    bad.fill_bytes(0xff);
+    k_validate<<<nblocks(n, 256), 256, 0, s>>>(n, pos, sto ? f : nullptr, str ? h : nullptr,
+                                                str ? nu : nullptr, str ? 1 : 0, bad.get());
+    ST_LAUNCH("k_validate");
+    count_launch();
+    unsigned long long hb[5];
+    ST_CUDA(cudaMemcpyAsync(hb, bad.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    const char* names[4] = {"position", "force_weight", "dipole_weight", "normal"};
+    for (int k = 0; k < 4; ++k)
+        if (hb[k] != ~0ull)
+            fail(ST_INVALID_ARGUMENT, std::string("particle array '") + names[k] + "' contains a non-finite value");
+    if (hb[4] != ~0ull) fail(ST_INVALID_ARGUMENT, "normal " + std::to_string(hb[4]) + " is not unit length");
+}
+
+// ------------------------------------------------------------ device-resident inputs
+struct DevParticles {
+    size_t n = 0;
+    const double *pos = nullptr, *f = nullptr, *h = nullptr, *nu = nullptr;
+    DevArray<double> own_pos, own_f, own_h, own_nu;
+};
+
+void upload(const st_particles* ps, bool need_f, bool need_hn, DevParticles& d, cudaStream_t s) {
+    d.n = ps->n;
+    auto up = [&](const double* src, DevArray<double>& dst) -> const double* {
+        if (!src) return nullptr;
+        dst.alloc(3 * ps->n, s);
+        ST_CUDA(cudaMemcpyAsync(dst.get(), src, 3 * ps->n * sizeof(double), cudaMemcpyHostToDevice, s));
+        return dst.get();
+    };
+    d.pos = up(ps->position, d.own_pos);
+    d.f = need_f ? up(ps->force_weight, d.own_f) : nullptr;
+    d.h = need_hn ? up(ps->dipole_weight, d.own_h) : nullptr;
+    d.nu = need_hn ? up(ps->normal, d.own_nu) : nullptr;
+}
+
+// ------------------------------------------------------------ the treecode
+struct RunOut {
+    uint64_t stats[3] = {0, 0, 0};
+    double t_build = 0, t_moments = 0, t_traverse = 0, t_total = 0, t_far = 0, t_near = 0;
+};
+
+void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
+
+void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in, const st_params& prm,
+                  double* d_out, uint64_t* d_per_target, int shard, int nshards, cudaStream_t s,
+                  RunOut& ro) {
+    const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
+    const size_t n = src.n;
+    const bool same = d_targets == nullptr;
+    const size_t nt = same ? n : nt_in;
+    if (nt >= 0x7fffffffull - 64) fail(ST_INVALID_ARGUMENT, "too many targets");
+    Event e0, e1, e2, e3, ef0, ef1, en1;
+    e0.record(s);
+
+    // K1: tree over the sources, tree-ordered source records
+    DevTree tree;
+    build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    DevArray<double> rec(12 * n, s);
+    DevArray<uint32_t> to_tree(n, s);
+    k_pack<<<nblocks(n, 256), 256, 0, s>>>(n, tree.perm.get(), src.pos, sto ? src.f : nullptr,
+                                           str ? src.h : nullptr, str ? src.nu : nullptr, rec.get(),
+                                           to_tree.get());
+    ST_LAUNCH("k_pack");
+    count_launch();
+    e1.record(s);
+
+    // K2: moments at order p, folded into the harmonic far-field weights
+    DevArray<double> M, W;
+    compute_moments_device(tree, rec.get(), prm.order, sto, str, s, M);
+    fold_weights_device(M.get(), tree.ncl, prm.order, sto, str, s, W);
+    M.reset();
+    e2.record(s);
+
+    // batch order of the targets: a leaf-capacity-32 octree over the target points
+    const double* tpos = same ? src.pos : d_targets;
+    DevTree ttree;
+    build_tree_device(tpos, nt, 32, false, false, s, ttree);
+    DevArray<double> tx(3 * nt, s), ufar(3 * nt, s);
+    DevArray<uint32_t> torig(nt, s), tskip(nt, s);
+    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, ttree.perm.get(), tpos, same ? to_tree.get() : nullptr,
+                                               tx.get(), torig.get(), tskip.get());
+    ST_LAUNCH("k_targets");
+    count_launch();
+
+    DevArray<unsigned long long> d_stats(3, s);
+    DevArray<int> d_err(1, s);
+    d_stats.zero();
+    d_err.zero();
+
+    TravArgs a;
+    a.tx = tx.get();
+    a.tskip = tskip.get();
+    a.torig = torig.get();
+    a.nt = (int)nt;
+    const int nwarps = (int)((nt + 31) / 32);
+    a.w0 = 0;
+    a.w1 = nwarps;
+    a.geom = tree.geom.get();
+    a.info = tree.info.get();
+    a.ncl = tree.ncl;
+    a.th2 = prm.theta * prm.theta;
+    a.W = W.get();
+    a.src = rec.get();
+    a.ufar = ufar.get();
+    a.out = d_out;
+    a.per_target = d_per_target;
+    a.stats = d_stats.get();
+    a.err = d_err.get();
+    const int P = prm.order + (str ? 2 : 1);
+
+    if (nshards > 1) {
+        // work-balanced contiguous warp ranges, identical on every rank (deterministic)
+        DevArray<float> cost(nwarps, s);
+        a.warp_cost = cost.get();
+        const float cf = (float)((P + 1) * (P + 1) * 10), cn = 32.f;
+        launch_count(a, cf, cn, s);
+        std::vector<float> hc(nwarps);
+        ST_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), sizeof(float) * nwarps, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        std::vector<double> w(hc.begin(), hc.end());
+        std::vector<size_t> cuts(nshards + 1);
+        shard_cuts_host(nwarps, w.data(), nshards, cuts.data());
+        a.w0 = (int)cuts[shard];
+        a.w1 = (int)cuts[shard + 1];
+        a.warp_cost = nullptr;
+    }
+
+    ef0.record(s);
+    launch_far(P, a, s);
+    ef1.record(s);
+    launch_near(sto, str, a, s);
+    en1.record(s);
+    e3.record(s);
+
+    int herr = 0;
+    ST_CUDA(cudaMemcpyAsync(&herr, d_err.get(), sizeof herr, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(ro.stats, d_stats.get(), sizeof ro.stats, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    if (herr) fail(ST_DOMAIN_ERROR, "direct sum: coincident particles");
+    ro.t_build = secs(e0, e1);
+    ro.t_moments = secs(e1, e2);
+    ro.t_traverse = secs(e2, e3);
+    ro.t_total = secs(e0, e3);
+    ro.t_far = secs(ef0, ef1);
+    ro.t_near = secs(ef1, en1);
+}
+
+void fill_stats(st_stats* st, const RunOut& ro) {
+    if (!st) return;
+    st->farfield_evals = ro.stats[0];
+    st->direct_pairs = ro.stats[1];
+    st->clusters_visited = ro.stats[2];
+    st->time_build_s = ro.t_build;
+    st->time_moments_s = ro.t_moments;
+    st->time_traverse_s = ro.t_traverse;
+    st->time_total_s = ro.t_total;
+    st->time_far_s = ro.t_far;
+    st->time_near_s = ro.t_near;
+}
+
+void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts) {
+    double total = 0.0;
+    for (size_t i = 0; i < n; ++i) total += w[i] > 0 ? w[i] : 0.0;
+    cuts[0] = 0;
+    double run = 0.0;
+    size_t i = 0;
+    for (int sIdx = 1; sIdx < k; ++sIdx) {
+        const double target = total * sIdx / k;
+        while (i < n && run + 0.5 * (w[i] > 0 ? w[i] : 0.0) < target) {
+            run += w[i] > 0 ? w[i] : 0.0;
+            ++i;
+        }
+        cuts[sIdx] = std::max(cuts[sIdx - 1], i);
+    }
+    cuts[k] = n;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+struct st_tree {
+    OwnedStream own;  // declared first: destroyed after the arrays that free on it
+    DevTree tree;
+    DevArray<double> rec;  // tree-ordered source records (ClusterTree::particles)
+    size_t n = 0;
+    bool sto = false, str = false;
+    cudaStream_t s = nullptr;
+};
+
+extern "C" {
+
+int st_abi_version(void) { return ST_ABI_VERSION; }
+
+const char* st_last_error(void) { return g_last_error.c_str(); }
+
+st_status st_device_count(int* out) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    if (out) *out = n;
+    return ST_OK;
+}
+
+st_status st_params_validate(const st_params* p) {
+    return guarded([&] { validate_params(p); });
+}
+
+st_status st_treecode_velocity_ex(const st_particles* src, const double* targets, size_t n_targets,
+                                  const st_params* params, double* u_out, uint64_t* per_target,
+                                  st_stats* stats) {
+    return guarded([&] {
+        g_launches = 0;
+        validate_params(params);
+        const bool sto = params->stokeslet != 0, str = params->stresslet != 0;
+        validate_shape(src, sto, str);
+        if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
+        if (!u_out) fail(ST_INVALID_ARGUMENT, "u_out: null");
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        Event h0, h1, d0, d1;
+        h0.record(s);
+        DevParticles d;
+        upload(src, sto, str, d, s);
+        const size_t nt = targets ? n_targets : src->n;
+        DevArray<double> dt;
+        if (targets) {
+            dt.alloc(3 * nt, s);
+            ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        h1.record(s);
+        validate_values_device(d.n, d.pos, d.f, d.h, d.nu, sto, str, s);
+        if (targets) {
+            DevArray<unsigned long long> bad(5, s);
+            bad.fill_bytes(0xff);
+            k_validate<<<nblocks(nt, 256), 256, 0, s>>>(nt, dt.get(), nullptr, nullptr, nullptr, 0, bad.get());
+            ST_LAUNCH("k_validate");
+            unsigned long long hb = 0;
+            ST_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
+            ST_CUDA(cudaStreamSynchronize(s));
+            if (hb != ~0ull) fail(ST_INVALID_ARGUMENT, "targets: non-finite position");
+        }
+        DevArray<double> du(3 * nt, s);
+        DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s);
+        RunOut ro;
+        run_treecode(d, targets ? dt.get() : nullptr, nt, *params, du.get(), per_target ? dpt.get() : nullptr, 0,
+                     1, s, ro);
+        d0.record(s);
+        ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (per_target)
+            ST_CUDA(cudaMemcpyAsync(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        d1.record(s);
+        ST_CUDA(cudaStreamSynchronize(s));
+        fill_stats(stats, ro);
+        if (stats) {
+            stats->time_h2d_s = secs(h0, h1);
+            stats->time_d2h_s = secs(d0, d1);
+            stats->gpu_launches = g_launches;
+        }
+    });
+}
+
+st_status st_treecode_velocity(const st_particles* src, const st_params* params, double* u_out,
+                               st_stats* stats) {
+    return st_treecode_velocity_ex(src, nullptr, 0, params, u_out, nullptr, stats);
+}
+
+st_status st_treecode_velocity_device(const st_particles* src, const double* targets, size_t n_targets,
+                                      const st_params* params, double* u_out, int shard, int n_shards,
+                                      void* stream, st_stats* stats) {
+    return guarded([&] {
+        g_launches = 0;
+        validate_params(params);
+        const bool sto = params->stokeslet != 0, str = params->stresslet != 0;
+        validate_shape(src, sto, str);
+        if (n_shards < 1 || shard < 0 || shard >= n_shards) fail(ST_INVALID_ARGUMENT, "shard out of range");
+        if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevParticles d;
+        d.n = src->n;
+        d.pos = src->position;
+        d.f = sto ? src->force_weight : nullptr;
+        d.h = str ? src->dipole_weight : nullptr;
+        d.nu = str ? src->normal : nullptr;
+        validate_values_device(d.n, d.pos, d.f, d.h, d.nu, sto, str, s);
+        RunOut ro;
+        run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro);
+        fill_stats(stats, ro);
+        if (stats) stats->gpu_launches = g_launches;
+    });
+}
+
+static void direct_common(const st_particles* src, int sto, int str, const std::vector<int64_t>& tg,
+                          double* u_out, bool naive) {
+    validate_shape(src, sto != 0, str != 0);
+    ensure_device();
+    OwnedStream os;
+    cudaStream_t s = os.s;
+    DevParticles d;
+    upload(src, sto != 0, str != 0, d, s);
+    validate_values_device(d.n, d.pos, d.f, d.h, d.nu, sto != 0, str != 0, s);
+    DevArray<double> rec(12 * d.n, s);
+    k_pack<<<nblocks(d.n, 256), 256, 0, s>>>(d.n, nullptr, d.pos, d.f, d.h, d.nu, rec.get(), nullptr);
+    ST_LAUNCH("k_pack");
+    DevArray<int> err(1, s);
+    err.zero();
+    const size_t nt = naive ? d.n : tg.size();
+    DevArray<double> du(3 * std::max<size_t>(nt, 1), s);
+    if (naive) {
+        launch_naive(sto != 0, str != 0, rec.get(), d.n, du.get(), err.get(), s);
+    } else if (nt) {
+        DevArray<int64_t> dtg(nt, s);
+        ST_CUDA(cudaMemcpyAsync(dtg.get(), tg.data(), nt * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        launch_direct(sto != 0, str != 0, rec.get(), d.n, dtg.get(), nt, du.get(), err.get(), s);
+    }
+    int herr = 0;
+    ST_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof herr, cudaMemcpyDeviceToHost, s));
+    if (nt) ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    if (herr)
+        fail(ST_DOMAIN_ERROR, naive ? "stokeslet: coincident points" : "direct sum: coincident particles");
+}
+
+st_status st_direct_velocity(const st_particles* src, int sto, int str, size_t first, size_t last,
+                             double* u_out) {
+    return guarded([&] {
+        validate_shape(src, sto != 0, str != 0);
+        if (first > last || last > src->n)
+            fail(ST_INVALID_ARGUMENT, "contracted_direct_velocity: bad target range");
+        std::vector<int64_t> tg(last - first);
+        for (size_t i = first; i < last; ++i) tg[i - first] = (int64_t)i;
+        direct_common(src, sto, str, tg, u_out, false);
+    });
+}
+
+st_status st_direct_velocity_at(const st_particles* src, int sto, int str, const size_t* targets,
+                                size_t n_targets, double* u_out) {
+    return guarded([&] {
+        validate_shape(src, sto != 0, str != 0);
+        std::vector<int64_t> tg(n_targets);
+        for (size_t i = 0; i < n_targets; ++i) {
+            if (targets[i] >= src->n)
+                fail(ST_INVALID_ARGUMENT, "contracted_direct_velocity_at: target out of range");
+            tg[i] = (int64_t)targets[i];
+        }
+        direct_common(src, sto, str, tg, u_out, false);
+    });
+}
+
+st_status st_naive_direct_velocity(const st_particles* src, int sto, int str, double* u_out) {
+    return guarded([&] { direct_common(src, sto, str, {}, u_out, true); });
+}
+
+st_status st_build_tree(const st_particles* src, int leaf_capacity, int shrink, st_tree** out) {
+    return guarded([&] {
+        if (!out) fail(ST_INVALID_ARGUMENT, "build_tree: null output");
+        *out = nullptr;
+        if (!src || src->n == 0) fail(ST_INVALID_ARGUMENT, "build_tree: empty particle set");
+        if (!src->position) fail(ST_INVALID_ARGUMENT, "build_tree: null positions");
+        if (leaf_capacity < 1) fail(ST_INVALID_ARGUMENT, "build_tree: leaf capacity must be >= 1");
+        ensure_device();
+        auto* t = new st_tree();
+        try {
+            t->s = t->own.s;
+            t->n = src->n;
+            t->sto = src->force_weight != nullptr;
+            t->str = src->dipole_weight != nullptr && src->normal != nullptr;
+            DevParticles d;
+            upload(src, t->sto, t->str, d, t->s);
+            build_tree_device(d.pos, d.n, leaf_capacity, shrink != 0, true, t->s, t->tree);
+            t->rec.alloc(12 * d.n, t->s);
+            k_pack<<<nblocks(d.n, 256), 256, 0, t->s>>>(d.n, t->tree.perm.get(), d.pos, d.f, d.h, d.nu,
+                                                        t->rec.get(), nullptr);
+            ST_LAUNCH("k_pack");
+            ST_CUDA(cudaStreamSynchronize(t->s));
+        } catch (...) {
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+
+size_t st_tree_num_clusters(const st_tree* t) { return t ? (size_t)t->tree.ncl : 0; }
+size_t st_tree_num_particles(const st_tree* t) { return t ? t->n : 0; }
+
+st_status st_tree_export(const st_tree* t, int64_t* begin_end, double* geom, int32_t* children,
+                         int32_t* meta, uint32_t* to_original) {
+    return guarded([&] {
+        if (!t) fail(ST_INVALID_ARGUMENT, "tree: null");
+        const int ncl = t->tree.ncl;
+        cudaStream_t s = t->s;
+        std::vector<int4> info(ncl);
+        std::vector<double4> g(ncl);
+        std::vector<double> bb(6 * (size_t)ncl);
+        std::vector<int32_t> ch(8 * (size_t)ncl), nch(ncl);
+        ST_CUDA(cudaMemcpyAsync(info.data(), t->tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaMemcpyAsync(g.data(), t->tree.geom.get(), sizeof(double4) * ncl, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaMemcpyAsync(bb.data(), t->tree.bbox.get(), sizeof(double) * 6 * ncl, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaMemcpyAsync(ch.data(), t->tree.children.get(), sizeof(int32_t) * 8 * ncl,
+                                cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaMemcpyAsync(nch.data(), t->tree.nchild.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
+        if (to_original)
+            ST_CUDA(cudaMemcpyAsync(to_original, t->tree.perm.get(), sizeof(uint32_t) * t->n,
+                                    cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        for (int v = 0; v < ncl; ++v) {
+            if (begin_end) {
+                begin_end[2 * v] = info[v].x;
+                begin_end[2 * v + 1] = info[v].y;
+            }
+            if (geom) {
+                double* q = geom + 10 * (size_t)v;
+                q[0] = g[v].x;
+                q[1] = g[v].y;
+                q[2] = g[v].z;
+                q[3] = g[v].w;
+                for (int a = 0; a < 6; ++a) q[4 + a] = bb[6 * (size_t)v + a];
+            }
+            if (children)
+                for (int j = 0; j < 8; ++j) children[8 * (size_t)v + j] = ch[8 * (size_t)v + j];
+            if (meta) {
+                meta[2 * v] = nch[v];
+                meta[2 * v + 1] = info[v].w;
+            }
+        }
+    });
+}
+
+void st_tree_free(st_tree* t) { delete t; }
+
+st_status st_compute_moments(const st_tree* t, int order, int sto, int str, double* stok, double* strm,
+                             double* trace, double* sym) {
+    return guarded([&] {
+        if (!t) fail(ST_INVALID_ARGUMENT, "tree: null");
+        if (order < 0 || order > 16) fail(ST_INVALID_ARGUMENT, "compute_moments: order outside table range");
+        if (!sto && !str) fail(ST_INVALID_ARGUMENT, "kernel selection: at least one kernel must be enabled");
+        if ((sto && !t->sto) || (str && !t->str))
+            fail(ST_INVALID_ARGUMENT, "compute_moments: tree was built without the weights of this kernel");
+        cudaStream_t s = t->s;
+        DevArray<double> M;
+        compute_moments_device(t->tree, t->rec.get(), order, sto != 0, str != 0, s, M);
+        const size_t E = mi_count(order), ncl = t->tree.ncl;
+        DevArray<double> a(sto ? 3 * E * ncl : 0, s), b(str ? 9 * E * ncl : 0, s), c(str ? E * ncl : 0, s),
+            d(str ? 6 * E * ncl : 0, s);
+        export_moments_device(M.get(), (int)ncl, order, sto != 0, str != 0, a.get(), b.get(), c.get(), d.get(), s);
+        auto down = [&](double* h, const DevArray<double>& x) {
+            if (h && x.size()) ST_CUDA(cudaMemcpyAsync(h, x.get(), x.bytes(), cudaMemcpyDeviceToHost, s));
+        };
+        down(stok, a);
+        down(strm, b);
+        down(trace, c);
+        down(sym, d);
+        ST_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+st_status st_coulomb_coeffs(size_t n, const double* dx, int pmax, double* b_out) {
+    return guarded([&] {
+        if (pmax < 0) fail(ST_INVALID_ARGUMENT, "MultiIndexTable: pmax must be >= 0");
+        for (size_t i = 0; i < n; ++i) {
+            const double r2 = dx[3 * i] * dx[3 * i] + dx[3 * i + 1] * dx[3 * i + 1] + dx[3 * i + 2] * dx[3 * i + 2];
+            if (!(r2 > 0.0)) fail(ST_DOMAIN_ERROR, "coulomb_coeffs: zero displacement");
+        }
+        if (!n) return;
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        const size_t E = mi_count(pmax);
+        DevArray<double> ddx(3 * n, s), db(E * n, s);
+        ST_CUDA(cudaMemcpyAsync(ddx.get(), dx, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_coulomb(n, ddx.get(), pmax, db.get(), s);
+        ST_CUDA(cudaMemcpyAsync(b_out, db.get(), db.bytes(), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+st_status st_farfield_pairs(size_t n, const double* dx, int order, int sto, int str, const double* stok,
+                            const double* strm, const double* /*trace*/, const double* /*sym*/,
+                            double* u_out) {
+    return guarded([&] {
+        if (order < 0 || order > 16) fail(ST_INVALID_ARGUMENT, "farfield: order out of range");
+        if (!sto && !str) fail(ST_INVALID_ARGUMENT, "kernel selection: at least one kernel must be enabled");
+        if ((sto && !stok) || (str && !strm)) fail(ST_INVALID_ARGUMENT, "farfield: moment order mismatch");
+        for (size_t i = 0; i < n; ++i) {
+            const double r2 = dx[3 * i] * dx[3 * i] + dx[3 * i + 1] * dx[3 * i + 1] + dx[3 * i + 2] * dx[3 * i + 2];
+            if (!(r2 > 0.0)) fail(ST_DOMAIN_ERROR, "coulomb_coeffs: zero displacement");
+        }
+        if (!n) return;
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        const size_t E = mi_count(order);
+        DevArray<double> ddx(3 * n, s), a(sto ? 3 * E * n : 0, s), b(str ? 9 * E * n : 0, s), M(12 * E * n, s), W,
+            du(3 * n, s);
+        ST_CUDA(cudaMemcpyAsync(ddx.get(), dx, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (sto) ST_CUDA(cudaMemcpyAsync(a.get(), stok, a.bytes(), cudaMemcpyHostToDevice, s));
+        if (str) ST_CUDA(cudaMemcpyAsync(b.get(), strm, b.bytes(), cudaMemcpyHostToDevice, s));
+        import_moments_device((int)n, order, sto != 0, str != 0, a.get(), b.get(), M.get(), s);
+        fold_weights_device(M.get(), (int)n, order, sto != 0, str != 0, s, W);
+        launch_far_pairs(order + (str ? 2 : 1), n, ddx.get(), W.get(), du.get(), s);
+        ST_CUDA(cudaMemcpyAsync(u_out, du.get(), du.bytes(), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+st_status st_relative_error(size_t n, const double* u_ref, const double* u_test, double* out) {
+    return guarded([&] {
+        if (n == 0) fail(ST_INVALID_ARGUMENT, "relative_error: empty fields");
+        double num = 0.0, den = 0.0;
+        for (size_t i = 0; i < n; ++i) {
+            const double* a = u_ref + 3 * i;
+            const double* b = u_test + 3 * i;
+            const double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
+            num += d0 * d0 + d1 * d1 + d2 * d2;
+            den += a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+        }
+        if (den == 0.0) fail(ST_DOMAIN_ERROR, "relative_error: reference field is identically zero");
+        *out = std::sqrt(num / den);
+    });
+}
+
+st_status st_shard_cuts(size_t n_units, const double* weights, int n_shards, size_t* cuts) {
+    return guarded([&] {
+        if (n_shards < 1) fail(ST_INVALID_ARGUMENT, "shard_cuts: n_shards must be >= 1");
+        if (!cuts || (n_units && !weights)) fail(ST_INVALID_ARGUMENT, "shard_cuts: null buffer");
+        shard_cuts_host(n_units, weights, n_shards, cuts);
+    });
+}
+
+st_status st_fp64_peak(double seconds, double* tflops) {
+    return guarded([&] {
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        int dev = 0, nsm = 0;
+        ST_CUDA(cudaGetDevice(&dev));
+        ST_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        DevArray<double> sink(1, s);
+        const int blocks = nsm * 8, threads = 256;
+        Event a, b;
+        int iters = 256;
+        double t = 0.0;
+        for (;;) {
+            a.record(s);
+            k_fp64_peak<<<blocks, threads, 0, s>>>(sink.get(), iters, 1.0);
+            ST_LAUNCH("k_fp64_peak");
+            b.record(s);
+            ST_CUDA(cudaStreamSynchronize(s));
+            t = secs(a, b);
+            if (t >= seconds || iters > (1 << 24)) break;
+            iters *= std::max(2, (int)std::min(16.0, seconds / std::max(t, 1e-6)));
+        }
+        const double fmas = (double)blocks * threads * iters * 16.0 * 8.0;
+        *tflops = 2.0 * fmas / t * 1e-12;
+    });
+}
+
+}  // extern "C"

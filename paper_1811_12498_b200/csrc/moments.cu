@@ -1,0 +1,421 @@
+// K2: moments of every cluster directly from its particles (moments.hpp:34-80,
+// compute_moments :140-175), then the fold into far-field weights.
+//
+// Moments: one CTA per (cluster, chunk of <= kChunk particles).  Particles of a
+// tile are staged in shared memory as powers d_a^0..d_a^p per axis plus their
+// 12 weights (f, h (x) nu); thread e owns multi-indices e, e+256, ... and
+// accumulates mono_k * w for every weight column.  Clusters spanning several
+// chunks write per-chunk partials that a second kernel sums in chunk order, so
+// the result is deterministic and identical on every GPU.
+//
+// Fold: the reference's contracted far fields (farfield.hpp
+// Eq. 25 / Eq. 30) equal sum_k a^k_ij M_j^k + a~^k_ijl M~_jl^k with the exact
+// Taylor coefficients a, a~ (taylor_coeffs.hpp:13-46).  Writing S and T with the
+// free index carried by (x - y)_i gives u_i = Phi_i(dx) + dx_i Psi(dx) with four
+// harmonic potentials, Phi_i = sum_q b_q alpha_i[q], Psi = sum_q b_q psi[q]:
+//   Stokeslet, per k (|k| <= p):
+//     alpha_i[k]          += (1 - k_i) M_i^k
+//     alpha_i[k+e_j-e_i]  -= (k_j + 1) M_j^k            (j != i)
+//     psi[k+e_j]          += (k_j + 1) M_j^k
+//   stresslet:
+//     psi[k+e_j+e_l]      += (k_j+1)(k_l+1+d_jl) M~_jl^k / 3
+//     alpha_i[k-e_i+e_j+e_l] -= k_i (m!/k!) M~_jl^k / 3  (m = k-e_i+e_j+e_l)
+//     alpha_i[k+e_i]      += (k_i + 1) tr(M~^k) / 3
+// and, because 1/r is harmonic (sum_i (k_i+1)(k_i+2) b^{k+2e_i} = 0), every
+// weight at k3 >= 2 is folded onto k3 - 2 until only k3 in {0,1} remain:
+// (P+1)^2 coefficients instead of E(P).
+#include <algorithm>
+
+#include "moments.cuh"
+
+namespace st {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTileP = 32;      // particles per shared-memory tile
+constexpr int kChunk = 8192;    // particles per work item
+constexpr int kPmax = 16;
+constexpr int kPow = kPmax + 1; // powers 0..p per axis
+
+__device__ __forceinline__ int find_item(const int32_t* __restrict__ off, int n, int item) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= item) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// flat graded-lex index -> (k1,k2,k3) (multi_index.hpp:36-44)
+__device__ __forceinline__ void mi_decode(int e, int& k1, int& k2, int& k3) {
+    int s = 0;
+    while (mi_count(s) <= e) ++s;
+    int r = e - (s == 0 ? 0 : mi_count(s - 1));
+    k1 = 0;
+    while (r >= s - k1 + 1) {
+        r -= s - k1 + 1;
+        ++k1;
+    }
+    k2 = r;
+    k3 = s - k1 - k2;
+}
+
+template <int EPT, bool STO, bool STR>
+__global__ void __launch_bounds__(kThreads)
+    k_moments(int ncl_items, const int32_t* __restrict__ item_off, const int32_t* __restrict__ item_cl,
+              int nmulti, const int4* __restrict__ info, const double4* __restrict__ geom,
+              const double* __restrict__ src, int p, int E, const int32_t* __restrict__ part_slot,
+              double* __restrict__ M, double* __restrict__ part) {
+    constexpr int NC = (STO ? 3 : 0) + (STR ? 9 : 0);
+    constexpr int C0 = STO ? 0 : 3;  // first combined column written
+    __shared__ double s_pow[kTileP][3 * kPow + 1];
+    __shared__ double s_w[kTileP][NC];
+    __shared__ int s_k[EPT * kThreads][3];
+
+    const int item = blockIdx.x;
+    const int ci = find_item(item_off, ncl_items, item);  // index into the cluster list
+    const int v = item_cl[ci];
+    const int chunk = item - item_off[ci];
+    const int4 inf = info[v];
+    const double4 g = geom[v];
+    const int b = inf.x + chunk * kChunk;
+    const int e_end = min(inf.y, b + kChunk);
+
+    for (int t = threadIdx.x; t < EPT * kThreads; t += kThreads) {
+        int k1 = 0, k2 = 0, k3 = 0;
+        if (t < E) mi_decode(t, k1, k2, k3);
+        s_k[t][0] = k1;
+        s_k[t][1] = k2;
+        s_k[t][2] = k3;
+    }
+
+    double acc[EPT][NC];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[j][c] = 0.0;
+
+    for (int t0 = b; t0 < e_end; t0 += kTileP) {
+        const int nt = min(kTileP, e_end - t0);
+        __syncthreads();
+        if (threadIdx.x < nt) {
+            const double* r = src + 12 * (size_t)(t0 + threadIdx.x);
+            const double d[3] = {r[0] - g.x, r[1] - g.y, r[2] - g.z};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                double pw = 1.0;
+                s_pow[threadIdx.x][a * kPow] = 1.0;
+                for (int q = 1; q <= p; ++q) {
+                    pw *= d[a];
+                    s_pow[threadIdx.x][a * kPow + q] = pw;
+                }
+            }
+            if (STO)
+                for (int c = 0; c < 3; ++c) s_w[threadIdx.x][c] = r[3 + c];
+            if (STR)
+                for (int j = 0; j < 3; ++j)
+                    for (int l = 0; l < 3; ++l)
+                        s_w[threadIdx.x][(STO ? 3 : 0) + 3 * j + l] = r[6 + j] * r[9 + l];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+            const int e = threadIdx.x + j * kThreads;
+            const int k1 = s_k[e][0], k2 = s_k[e][1], k3 = s_k[e][2];
+            for (int q = 0; q < nt; ++q) {
+                const double mono = s_pow[q][k1] * s_pow[q][kPow + k2] * s_pow[q][2 * kPow + k3];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) acc[j][c] = fma(mono, s_w[q][c], acc[j][c]);
+            }
+        }
+    }
+    const int slot = part_slot[ci];
+    double* out = slot < 0 ? M + (size_t)v * E * 12 : part + ((size_t)slot + chunk) * E * 12;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+        const int e = threadIdx.x + j * kThreads;
+        if (e < E) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) out[(size_t)e * 12 + C0 + c] = acc[j][c];
+        }
+    }
+}
+
+// Sum the chunk partials of multi-chunk clusters in chunk order.
+__global__ void k_reduce_parts(int ncl_items, const int32_t* __restrict__ item_off,
+                               const int32_t* __restrict__ item_cl, const int32_t* __restrict__ part_slot,
+                               int E, const double* __restrict__ part, double* __restrict__ M) {
+    const int ci = blockIdx.y;
+    const int slot = part_slot[ci];
+    if (slot < 0) return;
+    const int nch = item_off[ci + 1] - item_off[ci];
+    const int v = item_cl[ci];
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < E * 12; x += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < nch; ++c) s += part[((size_t)slot + c) * E * 12 + x];
+        M[(size_t)v * E * 12 + x] = s;
+    }
+}
+
+__device__ __forceinline__ double fact_ratio(int q, int k) {  // q!/k! for |q-k| small
+    double r = 1.0;
+    for (int t = k + 1; t <= q; ++t) r *= t;
+    for (int t = q + 1; t <= k; ++t) r /= t;
+    return r;
+}
+
+// One CTA per moment block: gather the 4 weight columns for every |q| <= P, fold
+// k3 >= 2 onto the harmonic basis, write W[blk][h][4].
+template <bool STO, bool STR>
+__global__ void __launch_bounds__(kThreads)
+    k_fold(int p, int P, const double* __restrict__ M, double* __restrict__ W) {
+    extern __shared__ double s_w[];  // [E(P)][4]
+    const int EP = mi_count(P);
+    const int E = mi_count(p);
+    const double* Mb = M + (size_t)blockIdx.x * E * 12;
+    const double third = 1.0 / 3.0;
+
+    for (int q = threadIdx.x; q < EP; q += blockDim.x) {
+        int qk[3];
+        mi_decode(q, qk[0], qk[1], qk[2]);
+        const int nq = qk[0] + qk[1] + qk[2];
+        double w4[4] = {0.0, 0.0, 0.0, 0.0};
+        if (STO) {
+            for (int i = 0; i < 3; ++i) {
+                if (nq <= p) {
+                    w4[i] += (1 - qk[i]) * Mb[(size_t)q * 12 + i];
+                    for (int j = 0; j < 3; ++j) {
+                        if (j == i || qk[j] < 1) continue;
+                        int k[3] = {qk[0], qk[1], qk[2]};
+                        k[j] -= 1;
+                        k[i] += 1;
+                        w4[i] -= qk[j] * Mb[(size_t)mi_flat(k[0], k[1], k[2]) * 12 + j];
+                    }
+                }
+            }
+            if (nq >= 1 && nq - 1 <= p)
+                for (int j = 0; j < 3; ++j) {
+                    if (qk[j] < 1) continue;
+                    int k[3] = {qk[0], qk[1], qk[2]};
+                    k[j] -= 1;
+                    w4[3] += qk[j] * Mb[(size_t)mi_flat(k[0], k[1], k[2]) * 12 + j];
+                }
+        }
+        if (STR) {
+            for (int i = 0; i < 3; ++i) {
+                if (nq >= 1 && nq - 1 <= p) {
+                    for (int j = 0; j < 3; ++j)
+                        for (int l = 0; l < 3; ++l) {
+                            int k[3] = {qk[0], qk[1], qk[2]};
+                            k[i] += 1;
+                            k[j] -= 1;
+                            k[l] -= 1;
+                            if (k[0] < 0 || k[1] < 0 || k[2] < 0 || k[i] < 1) continue;
+                            const double ratio = fact_ratio(qk[0], k[0]) * fact_ratio(qk[1], k[1]) *
+                                                 fact_ratio(qk[2], k[2]);
+                            w4[i] -= k[i] * ratio * third *
+                                     Mb[(size_t)mi_flat(k[0], k[1], k[2]) * 12 + 3 + 3 * j + l];
+                        }
+                    if (qk[i] >= 1) {
+                        int k[3] = {qk[0], qk[1], qk[2]};
+                        k[i] -= 1;
+                        const double* m = Mb + (size_t)mi_flat(k[0], k[1], k[2]) * 12 + 3;
+                        w4[i] += qk[i] * third * ((m[0] + m[4]) + m[8]);
+                    }
+                }
+            }
+            if (nq >= 2 && nq - 2 <= p)
+                for (int j = 0; j < 3; ++j)
+                    for (int l = 0; l < 3; ++l) {
+                        int k[3] = {qk[0], qk[1], qk[2]};
+                        k[j] -= 1;
+                        k[l] -= 1;
+                        if (k[0] < 0 || k[1] < 0 || k[2] < 0) continue;
+                        const double C = (double)(k[j] + 1) * (double)(k[l] + 1 + (j == l));
+                        w4[3] += C * third * Mb[(size_t)mi_flat(k[0], k[1], k[2]) * 12 + 3 + 3 * j + l];
+                    }
+        }
+        for (int c = 0; c < 4; ++c) s_w[4 * q + c] = w4[c];
+    }
+    // harmonic fold, highest k3 first: W[t] -= (t1-1)t1/((t3+2)(t3+1)) W[t-2e1+2e3]
+    //                                        + (t2-1)t2/((t3+2)(t3+1)) W[t-2e2+2e3]
+    for (int c3 = P; c3 >= 2; --c3) {
+        __syncthreads();
+        const int t3 = c3 - 2;
+        const int rem = P - t3;  // t1 + t2 <= rem
+        const int cnt = (rem + 1) * (rem + 2) / 2;
+        for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+            // enumerate (t1, t2) with t1 + t2 <= rem
+            int t1 = 0, r = x;
+            while (r >= rem - t1 + 1) {
+                r -= rem - t1 + 1;
+                ++t1;
+            }
+            const int t2 = r;
+            const int tf = mi_flat(t1, t2, t3);
+            const double den = (double)((t3 + 2) * (t3 + 1));
+            double acc[4] = {s_w[4 * tf], s_w[4 * tf + 1], s_w[4 * tf + 2], s_w[4 * tf + 3]};
+            if (t1 >= 2) {  // source q = t - 2e1 + 2e3, |q| = |t|
+                const int qf = mi_flat(t1 - 2, t2, t3 + 2);
+                const double cf = (double)((t1 - 1) * t1) / den;
+                for (int c = 0; c < 4; ++c) acc[c] -= cf * s_w[4 * qf + c];
+            }
+            if (t2 >= 2) {  // source q = t - 2e2 + 2e3
+                const int qf = mi_flat(t1, t2 - 2, t3 + 2);
+                const double cf = (double)((t2 - 1) * t2) / den;
+                for (int c = 0; c < 4; ++c) acc[c] -= cf * s_w[4 * qf + c];
+            }
+            for (int c = 0; c < 4; ++c) s_w[4 * tf + c] = acc[c];
+        }
+    }
+    __syncthreads();
+    const int H = harm_count(P);
+    double* Wb = W + (size_t)blockIdx.x * H * 4;
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+        int s = 0;
+        while ((s + 1) * (s + 1) <= h) ++s;
+        const int j = h - s * s;
+        int k1, k2, k3;
+        if (j <= s) { k1 = s - j; k2 = j; k3 = 0; }
+        else { k2 = j - s - 1; k1 = s - 1 - k2; k3 = 1; }
+        const int f = mi_flat(k1, k2, k3);
+        for (int c = 0; c < 4; ++c) Wb[4 * h + c] = s_w[4 * f + c];
+    }
+}
+
+__global__ void k_export(int nblk, int E, int sto, int str, const double* __restrict__ M,
+                         double* __restrict__ stok, double* __restrict__ strm, double* __restrict__ trace,
+                         double* __restrict__ sym) {
+    const size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (x >= (size_t)nblk * E) return;
+    const double* m = M + x * 12;
+    if (sto)
+        for (int j = 0; j < 3; ++j) stok[3 * x + j] = m[j];
+    if (str) {
+        const double* t = m + 3;
+        for (int q = 0; q < 9; ++q) strm[9 * x + q] = t[q];
+        trace[x] = t[0] + t[4] + t[8];
+        double* s6 = sym + 6 * x;  // sym_index (multi_index.hpp:163-166)
+        s6[0] = 2.0 * t[0];
+        s6[3] = 2.0 * t[4];
+        s6[5] = 2.0 * t[8];
+        s6[1] = t[1] + t[3];
+        s6[2] = t[2] + t[6];
+        s6[4] = t[5] + t[7];
+    }
+}
+
+__global__ void k_import(int nblk, int E, int sto, int str, const double* __restrict__ stok,
+                         const double* __restrict__ strm, double* __restrict__ M) {
+    const size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (x >= (size_t)nblk * E) return;
+    double* m = M + x * 12;
+    for (int j = 0; j < 3; ++j) m[j] = sto ? stok[3 * x + j] : 0.0;
+    for (int q = 0; q < 9; ++q) m[3 + q] = str ? strm[9 * x + q] : 0.0;
+}
+
+template <int EPT>
+void launch_moments_ept(bool sto, bool str, dim3 g, cudaStream_t s, int ncl_items, const int32_t* off,
+                        const int32_t* cl, int nmulti, const int4* info, const double4* geom,
+                        const double* src, int p, int E, const int32_t* slot, double* M, double* part) {
+    if (sto && str)
+        k_moments<EPT, true, true><<<g, kThreads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
+                                                          slot, M, part);
+    else if (sto)
+        k_moments<EPT, true, false><<<g, kThreads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
+                                                           slot, M, part);
+    else
+        k_moments<EPT, false, true><<<g, kThreads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
+                                                           slot, M, part);
+    ST_LAUNCH("k_moments");
+    count_launch();
+}
+
+}  // namespace
+
+void compute_moments_device(const DevTree& tree, const double* src, int p, bool sto, bool str,
+                            cudaStream_t s, DevArray<double>& M) {
+    if (p < 0 || p > kPmax) fail(ST_INVALID_ARGUMENT, "compute_moments: order outside table range");
+    const int E = mi_count(p);
+    const int ncl = tree.ncl;
+    // work items per cluster from the host copy of the cluster ranges
+    std::vector<int4> info(ncl);
+    ST_CUDA(cudaMemcpyAsync(info.data(), tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> off(ncl + 1), cl(ncl), slot(ncl);
+    int items = 0, parts = 0;
+    for (int v = 0; v < ncl; ++v) {
+        const int cnt = info[v].y - info[v].x;
+        const int nch = std::max(1, (cnt + kChunk - 1) / kChunk);
+        cl[v] = v;
+        off[v] = items;
+        slot[v] = nch > 1 ? parts : -1;
+        if (nch > 1) parts += nch;
+        items += nch;
+    }
+    off[ncl] = items;
+    DevArray<int32_t> d_off(ncl + 1, s), d_cl(ncl, s), d_slot(ncl, s);
+    ST_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), sizeof(int32_t) * (ncl + 1), cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_cl.get(), cl.data(), sizeof(int32_t) * ncl, cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(int32_t) * ncl, cudaMemcpyHostToDevice, s));
+    M.alloc((size_t)ncl * E * 12, s);
+    M.zero();
+    DevArray<double> part((size_t)std::max(parts, 1) * E * 12, s);
+    const int ept = (E + kThreads - 1) / kThreads;
+    dim3 g(items);
+    switch (ept) {
+        case 1: launch_moments_ept<1>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                      tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+        case 2: launch_moments_ept<2>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                      tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+        case 3: launch_moments_ept<3>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                      tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+        default: launch_moments_ept<4>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                       tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+    }
+    if (parts) {
+        k_reduce_parts<<<dim3(std::max(1, (E * 12 + 255) / 256), ncl), 256, 0, s>>>(
+            ncl, d_off.get(), d_cl.get(), d_slot.get(), E, part.get(), M.get());
+        ST_LAUNCH("k_reduce_parts");
+        count_launch();
+    }
+}
+
+void fold_weights_device(const double* M, int nblk, int p, bool sto, bool str, cudaStream_t s,
+                         DevArray<double>& W) {
+    const int P = p + (str ? 2 : 1);
+    const size_t smem = sizeof(double) * 4 * mi_count(P);
+    W.alloc((size_t)nblk * harm_count(P) * 4, s);
+    if (nblk == 0) return;
+    auto go = [&](auto kern) {
+        ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<nblk, kThreads, smem, s>>>(p, P, M, W.get());
+        ST_LAUNCH("k_fold");
+        count_launch();
+    };
+    if (sto && str) go(k_fold<true, true>);
+    else if (sto) go(k_fold<true, false>);
+    else go(k_fold<false, true>);
+}
+
+void export_moments_device(const double* M, int nblk, int p, bool sto, bool str, double* stok,
+                           double* strm, double* trace, double* sym, cudaStream_t s) {
+    const size_t n = (size_t)nblk * mi_count(p);
+    if (!n) return;
+    k_export<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nblk, mi_count(p), sto, str, M, stok, strm, trace, sym);
+    ST_LAUNCH("k_export");
+    count_launch();
+}
+
+void import_moments_device(int nblk, int p, bool sto, bool str, const double* stok, const double* strm,
+                           double* M, cudaStream_t s) {
+    const size_t n = (size_t)nblk * mi_count(p);
+    if (!n) return;
+    k_import<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nblk, mi_count(p), sto, str, stok, strm, M);
+    ST_LAUNCH("k_import");
+    count_launch();
+}
+
+}  // namespace st

@@ -1,0 +1,89 @@
+#include "scan.cuh"
+
+namespace st {
+
+namespace {
+constexpr int kScanThreads = 1024;
+
+// Block-wide inclusive scan of one value per thread (1024 threads).
+template <class T>
+__device__ T block_inclusive(T v, T* warp_sums) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) warp_sums[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        T w = warp_sums[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_sums[lane] = w;
+    }
+    __syncthreads();
+    if (wid > 0) v += warp_sums[wid - 1];
+    __syncthreads();
+    return v;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_cols(const uint32_t* __restrict__ in,
+                                                            uint32_t* __restrict__ out, int nrows,
+                                                            int ncols) {
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry;
+    for (int c = 0; c < ncols; ++c) {
+        if (threadIdx.x == 0) carry = 0;
+        __syncthreads();
+        for (int base = 0; base < nrows; base += kScanThreads) {
+            const int r = base + threadIdx.x;
+            const uint32_t v = r < nrows ? in[(size_t)r * ncols + c] : 0u;
+            const uint32_t inc = block_inclusive<uint32_t>(v, warp_sums);
+            const uint32_t cy = carry;
+            if (r < nrows) out[(size_t)r * ncols + c] = cy + inc - v;
+            __syncthreads();
+            if (threadIdx.x == kScanThreads - 1) carry = cy + inc;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[(size_t)nrows * ncols + c] = carry;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_i32(const int32_t* __restrict__ in,
+                                                           int32_t* __restrict__ out, int nrows) {
+    __shared__ int32_t warp_sums[32];
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nrows; base += kScanThreads) {
+        const int r = base + threadIdx.x;
+        const int32_t v = r < nrows ? in[r] : 0;
+        const int32_t inc = block_inclusive<int32_t>(v, warp_sums);
+        const int32_t cy = carry;
+        if (r < nrows) out[r] = cy + inc - v;
+        __syncthreads();
+        if (threadIdx.x == kScanThreads - 1) carry = cy + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[nrows] = carry;
+}
+
+void launch_scan_cols(const uint32_t* in, uint32_t* out, int nrows, int ncols, cudaStream_t s) {
+    k_scan_cols<<<1, kScanThreads, 0, s>>>(in, out, nrows, ncols);
+    ST_LAUNCH("k_scan_cols");
+    count_launch();
+}
+
+void launch_scan_i32(const int32_t* in, int32_t* out, int nrows, cudaStream_t s) {
+    k_scan_i32<<<1, kScanThreads, 0, s>>>(in, out, nrows);
+    ST_LAUNCH("k_scan_i32");
+    count_launch();
+}
+
+}  // namespace st

@@ -1,0 +1,112 @@
+// Shared host/device plumbing for the sm_100a treecode kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "stokestree_c.h"
+
+namespace st {
+
+// Error carrying the C-ABI status it maps to (ST_* in stokestree_c.h).
+struct Error : std::runtime_error {
+    st_status status;
+    Error(st_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(st_status s, const std::string& m) { throw Error(s, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(ST_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                                cudaGetErrorString(e) + ")");
+}
+#define ST_CUDA(call) ::st::cuda_check((call), #call)
+#define ST_LAUNCH(what) ::st::cuda_check(cudaGetLastError(), what)
+
+// Kernel-launch counter (reported as st_stats.gpu_launches).
+extern thread_local uint64_t g_launches;
+inline void count_launch(uint64_t k = 1) { g_launches += k; }
+
+// Stream-ordered device array (cudaMallocAsync on the device's default pool,
+// whose release threshold is raised once so memory is recycled across calls).
+template <class T>
+class DevArray {
+public:
+    DevArray() = default;
+    DevArray(size_t n, cudaStream_t s) { alloc(n, s); }
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept { swap(o); }
+    DevArray& operator=(DevArray&& o) noexcept {
+        if (this != &o) {
+            reset();
+            swap(o);
+        }
+        return *this;
+    }
+    ~DevArray() { reset(); }
+
+    void alloc(size_t n, cudaStream_t s) {
+        reset();
+        stream_ = s;
+        n_ = n;
+        if (n) ST_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    }
+    void reset() {
+        if (p_) cudaFreeAsync(p_, stream_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    void zero() {
+        if (n_) ST_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), stream_));
+    }
+    void fill_bytes(int v) {
+        if (n_) ST_CUDA(cudaMemsetAsync(p_, v, n_ * sizeof(T), stream_));
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    size_t bytes() const { return n_ * sizeof(T); }
+    T* release() {
+        T* p = p_;
+        p_ = nullptr;
+        n_ = 0;
+        return p;
+    }
+    void swap(DevArray& o) noexcept {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+        std::swap(stream_, o.stream_);
+    }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t stream_ = nullptr;
+};
+
+// Multi-index helpers shared by host and device.
+__host__ __device__ constexpr int mi_count(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
+// Graded-lex flat index (multi_index.hpp:36-44) of k with |k| = s:
+// offset(s) + position of (k1,k2) in the k1-major, k2-minor enumeration.
+__host__ __device__ inline int mi_flat(int k1, int k2, int k3) {
+    const int s = k1 + k2 + k3;
+    // entries before grade s: mi_count(s-1); within grade: k1 blocks of sizes (s+1), s, ...
+    const int before = s == 0 ? 0 : mi_count(s - 1);
+    // sum_{a<k1} (s - a + 1) = k1*(s+1) - k1*(k1-1)/2
+    return before + k1 * (s + 1) - k1 * (k1 - 1) / 2 + k2;
+}
+// Harmonic (k3 <= 1) basis index: grade s occupies [s^2, (s+1)^2): k3 = 0 entries
+// (s-j, j, 0) at j = 0..s, then k3 = 1 entries (s-1-j, j, 1) at s+1+j.
+__host__ __device__ inline int harm_index(int k1, int k2, int k3) {
+    const int s = k1 + k2 + k3;
+    return s * s + (k3 == 0 ? k2 : s + 1 + k2);
+}
+__host__ __device__ constexpr int harm_count(int P) { return (P + 1) * (P + 1); }
+
+}  // namespace st

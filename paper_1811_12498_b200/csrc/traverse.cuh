@@ -1,0 +1,50 @@
+// K3-K6: MAC traversal, far field, near field, O(N^2) direct sums.
+#pragma once
+
+#include "st_common.cuh"
+
+namespace st {
+
+constexpr uint32_t kNoSkip = 0xffffffffu;
+
+struct TravArgs {
+    const double* tx = nullptr;      // targets in batch (Morton) order, xyz
+    const uint32_t* tskip = nullptr; // source tree index excluded per target (kNoSkip: none)
+    const uint32_t* torig = nullptr; // original target index per batch position
+    int nt = 0;
+    int w0 = 0, w1 = 0;              // warp (32-target batch) range of this launch
+    const double4* geom = nullptr;   // pre-order clusters: centre, radius
+    const int4* info = nullptr;      // begin, end, next, is_leaf
+    int ncl = 0;
+    double th2 = 0.0;                // theta * theta
+    const double* W = nullptr;       // far weights [ncl][(P+1)^2][4]
+    const double* src = nullptr;     // tree-ordered source records [n][12]
+    double* ufar = nullptr;          // far-field sums per batch position [nt][3]
+    double* out = nullptr;           // final velocities, original target order [nt][3]
+    uint64_t* per_target = nullptr;  // optional {visited, far, direct}, original order
+    unsigned long long* stats = nullptr;  // {farfield_evals, direct_pairs, clusters_visited}
+    int* err = nullptr;              // set to 1 on a coincident source/target pair
+    float* warp_cost = nullptr;      // count pass: per-warp work estimate
+};
+
+// Far field for warps [w0, w1): P = p + 2 (stresslet) or p + 1.
+void launch_far(int P, const TravArgs& a, cudaStream_t s);
+// Near field + combine + scatter to original order + counters.
+void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s);
+// Traversal-only work estimate per warp (for multi-GPU shard cuts).
+void launch_count(const TravArgs& a, float far_cost, float near_cost, cudaStream_t s);
+
+// O(N^2) contracted direct sum (kernels.hpp:45-83, 123-150): sources are the
+// original-order records [n][12]; targets are source indices (self skipped).
+void launch_direct(bool sto, bool str, const double* rec, size_t n, const int64_t* tgt, size_t nt,
+                   double* u, int* err, cudaStream_t s);
+// naive_direct_velocity (kernels.hpp:89-118): tensors S, T formed per pair.
+void launch_naive(bool sto, bool str, const double* rec, size_t n, double* u, int* err,
+                  cudaStream_t s);
+
+// Per-pair far-field API: n pairs, pair i uses dx[3i..] and weight block i.
+void launch_far_pairs(int P, size_t n, const double* dx, const double* W, double* u, cudaStream_t s);
+// Reference-order Coulomb coefficients b^k, |k| <= pmax (coulomb.hpp:28-50).
+void launch_coulomb(size_t n, const double* dx, int pmax, double* b, cudaStream_t s);
+
+}  // namespace st

@@ -1,0 +1,646 @@
+// K1: level-synchronous device octree build, bit-exact with the reference's
+// recursive build_tree (cluster_tree.hpp:81-192).
+//
+// The reference recursion (pre-order emplace, geometric bisection with ties
+// going up, stable counting-sort scatter, empty children pruned, leaf iff
+// count <= N0 or depth >= 64) is equivalent to a breadth-first sequence of
+// stable 8-way partitions of every still-splitting segment: particles keep
+// their parent-range order inside each child, so the final order is the
+// reference's tree order.  Each level is
+//   seg_of -> slot + tile histogram -> column scan -> segment bases -> stable
+//   scatter -> children records -> compaction of the next active level,
+// followed by subtree sizes (bottom-up) and pre-order ids (top-down).
+// Geometry uses the reference's exact non-FMA expressions (__dadd_rn /
+// __dmul_rn), and min / max / max-of-norm2 are order-free exact reductions.
+#include <algorithm>
+#include <vector>
+
+#include "scan.cuh"
+#include "tree.cuh"
+
+namespace st {
+
+namespace {
+
+constexpr int kTile = 2048;      // elements per partition tile
+constexpr int kTileThreads = 256;
+constexpr int kGeomChunk = 4096; // elements per geometry work item
+
+__device__ __forceinline__ uint64_t ord_enc(double d) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_dec(uint64_t u) {
+    const uint64_t b = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+// norm2 as vec3.hpp:48-52 evaluates it: (a0*a0 + a1*a1) + a2*a2, no contraction.
+__device__ __forceinline__ double norm2_rn(double a0, double a1, double a2) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)), __dmul_rn(a2, a2));
+}
+
+template <class T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        T y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y < v ? y : v;
+    }
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        T y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = v < y ? y : v;
+    }
+    return v;
+}
+
+// tight box of all points (cluster_tree.hpp:58-69, 163) into ordered-int atomics.
+__global__ void k_tight_all(const double* __restrict__ pos, size_t n,
+                            unsigned long long* __restrict__ mm /* lo3 (min), hi3 (max) */) {
+    uint64_t lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const uint64_t e = ord_enc(pos[3 * i + a]);
+            lo[a] = e < lo[a] ? e : lo[a];
+            hi[a] = hi[a] < e ? e : hi[a];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = warp_min(lo[a]);
+        hi[a] = warp_max(hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&mm[a], (unsigned long long)lo[a]);
+            atomicMax(&mm[3 + a], (unsigned long long)hi[a]);
+        }
+    }
+}
+
+// Root cube (cluster_tree.hpp:163-169): side = max extent * (1 + 1e-12), centred
+// on the tight box.  Writes BFS node 0.
+__global__ void k_root(const unsigned long long* __restrict__ mm, uint32_t n, uint32_t* nb_begin,
+                       uint32_t* nb_end, double* nb_box) {
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = ord_dec(mm[a]);
+        hi[a] = ord_dec(mm[3 + a]);
+    }
+    double side = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        const double ext = __dsub_rn(hi[a], lo[a]);
+        side = side < ext ? ext : side;  // std::max(side, ext)
+    }
+    side = __dmul_rn(side, __dadd_rn(1.0, 1e-12));
+    const double half = __dmul_rn(side, 0.5);
+    for (int a = 0; a < 3; ++a) {
+        const double c = __dmul_rn(__dadd_rn(lo[a], hi[a]), 0.5);
+        nb_box[a] = __dsub_rn(c, half);
+        nb_box[3 + a] = __dadd_rn(c, half);
+    }
+    nb_begin[0] = 0;
+    nb_end[0] = n;
+}
+
+// Active segments of this level: range + geometric midpoint (cluster_tree.hpp:99).
+__global__ void k_mkseg(const int32_t* __restrict__ act, int m, const uint32_t* __restrict__ nb_begin,
+                        const uint32_t* __restrict__ nb_end, const double* __restrict__ nb_box,
+                        uint32_t* seg_begin, uint32_t* seg_end, double* seg_mid) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    const int v = act[s];
+    seg_begin[s] = nb_begin[v];
+    seg_end[s] = nb_end[v];
+    for (int a = 0; a < 3; ++a)
+        seg_mid[3 * s + a] = __dmul_rn(__dadd_rn(nb_box[6 * v + a], nb_box[6 * v + 3 + a]), 0.5);
+}
+
+// Element -> active segment (segments are disjoint and sorted by begin).
+__global__ void k_segof(uint32_t n, const uint32_t* __restrict__ seg_begin,
+                        const uint32_t* __restrict__ seg_end, int m, int32_t* __restrict__ seg_of) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int lo = 0, hi = m - 1, found = -1;
+    while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        if (seg_begin[mid] <= i) {
+            found = mid;
+            lo = mid + 1;
+        } else {
+            hi = mid - 1;
+        }
+    }
+    seg_of[i] = (found >= 0 && i < seg_end[found]) ? found : -1;
+}
+
+// Octant slot, ties go to the upper child (cluster_tree.hpp:101-105), and per-tile
+// histograms.  slot 8 marks elements outside every active segment.
+__global__ void __launch_bounds__(kTileThreads)
+    k_slot_hist(uint32_t n, const double* __restrict__ pos, const uint32_t* __restrict__ perm,
+                const int32_t* __restrict__ seg_of, const double* __restrict__ seg_mid,
+                uint8_t* __restrict__ slot8, uint32_t* __restrict__ blk_cnt) {
+    __shared__ uint32_t cnt[8];
+    if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t base = blockIdx.x * kTile;
+    for (int r = 0; r < kTile / kTileThreads; ++r) {
+        const uint32_t i = base + r * kTileThreads + threadIdx.x;
+        if (i >= n) break;
+        const int s = seg_of[i];
+        uint8_t slot = 8;
+        if (s >= 0) {
+            const double* p = pos + 3 * (size_t)perm[i];
+            const double* mid = seg_mid + 3 * s;
+            slot = (p[0] >= mid[0] ? 1 : 0) | (p[1] >= mid[1] ? 2 : 0) | (p[2] >= mid[2] ? 4 : 0);
+            atomicAdd(&cnt[slot], 1u);
+        }
+        slot8[i] = slot;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) blk_cnt[blockIdx.x * 8 + threadIdx.x] = cnt[threadIdx.x];
+}
+
+// Global exclusive per-slot prefix P[pos][k] at both ends of every active segment
+// (one warp per segment): seg_base[s][k] = P[begin][k], seg_cnt[s][k] = P[end][k] - P[begin][k].
+__global__ void k_segbase(int m, const uint32_t* __restrict__ seg_begin,
+                          const uint32_t* __restrict__ seg_end, const uint8_t* __restrict__ slot8,
+                          const uint32_t* __restrict__ blk_off, uint32_t* __restrict__ seg_base,
+                          uint32_t* __restrict__ seg_cnt) {
+    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= m) return;  // whole warps only; no block-level barrier below
+    uint32_t P[2] = {0, 0};
+    for (int which = 0; which < 2; ++which) {
+        const uint32_t p = which ? seg_end[s] : seg_begin[s];
+        const uint32_t tile = p / kTile;
+        uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t j = tile * kTile + lane; j < p; j += 32) {
+            const uint8_t k = slot8[j];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) c[q] += (k == q);
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) c[q] += __shfl_xor_sync(0xffffffffu, c[q], o);
+            if (q == lane) mine = c[q];
+        }
+        if (lane < 8) P[which] = blk_off[tile * 8 + lane] + mine;
+    }
+    if (lane < 8) {
+        seg_base[s * 8 + lane] = P[0];
+        seg_cnt[s * 8 + lane] = P[1] - P[0];
+    }
+}
+
+// Stable scatter: new position = segment begin + child offset + stable rank.
+__global__ void __launch_bounds__(kTileThreads)
+    k_scatter(uint32_t n, const uint8_t* __restrict__ slot8, const int32_t* __restrict__ seg_of,
+              const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ seg_begin,
+              const uint32_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_cnt,
+              const uint32_t* __restrict__ perm_in, uint32_t* __restrict__ perm_out) {
+    __shared__ uint32_t warp_cnt[kTileThreads / 32][8];
+    __shared__ uint32_t run[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x < 8) run[threadIdx.x] = 0;
+    const uint32_t base = blockIdx.x * kTile;
+    for (int r = 0; r < kTile / kTileThreads; ++r) {
+        const uint32_t i = base + r * kTileThreads + threadIdx.x;
+        const uint8_t slot = i < n ? slot8[i] : 8;
+        uint32_t rank_w = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const unsigned msk = __ballot_sync(0xffffffffu, slot == k);
+            if (lane == 0) warp_cnt[wid][k] = __popc(msk);
+            if (slot == k) rank_w = __popc(msk & lt);
+        }
+        __syncthreads();
+        uint32_t before = 0;
+        if (slot < 8) {
+            before = run[slot];
+            for (int w = 0; w < wid; ++w) before += warp_cnt[w][slot];
+        }
+        __syncthreads();
+        if (threadIdx.x < 8) {
+            uint32_t t = 0;
+            for (int w = 0; w < kTileThreads / 32; ++w) t += warp_cnt[w][threadIdx.x];
+            run[threadIdx.x] += t;
+        }
+        if (i < n) {
+            if (slot < 8) {
+                const int s = seg_of[i];
+                const uint32_t grank = blk_off[blockIdx.x * 8 + slot] + before + rank_w;
+                uint32_t child_off = 0;
+                for (int k = 0; k < slot; ++k) child_off += seg_cnt[s * 8 + k];
+                const uint32_t np = seg_begin[s] + child_off + (grank - seg_base[s * 8 + slot]);
+                perm_out[np] = perm_in[i];
+            } else {
+                perm_out[i] = perm_in[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_nch(int m, const uint32_t* __restrict__ seg_cnt, int32_t* __restrict__ nch) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    int c = 0;
+    for (int k = 0; k < 8; ++k) c += seg_cnt[s * 8 + k] != 0;
+    nch[s] = c;
+}
+
+// Child clusters in slot order (cluster_tree.hpp:125-137), empty slots pruned.
+__global__ void k_children(int m, const int32_t* __restrict__ act, const uint32_t* __restrict__ seg_begin,
+                           const uint32_t* __restrict__ seg_cnt, const int32_t* __restrict__ chbase,
+                           int next_start, int n0, int child_depth, const double* box_in,
+                           double* nb_box, uint32_t* __restrict__ nb_begin,
+                           uint32_t* __restrict__ nb_end, int32_t* __restrict__ nb_first,
+                           int32_t* __restrict__ nb_nch, int32_t* __restrict__ act_flag) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m) return;
+    const int v = act[s];
+    double glo[3], ghi[3], mid[3];
+    for (int a = 0; a < 3; ++a) {
+        glo[a] = box_in[6 * v + a];
+        ghi[a] = box_in[6 * v + 3 + a];
+        mid[a] = __dmul_rn(__dadd_rn(glo[a], ghi[a]), 0.5);
+    }
+    uint32_t off = seg_begin[s];
+    int c = next_start + chbase[s];
+    nb_first[v] = c;
+    nb_nch[v] = chbase[s + 1] - chbase[s];
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t cnt = seg_cnt[s * 8 + k];
+        if (!cnt) continue;
+        for (int a = 0; a < 3; ++a) {
+            const bool up = (k >> a) & 1;
+            nb_box[6 * c + a] = up ? mid[a] : glo[a];
+            nb_box[6 * c + 3 + a] = up ? ghi[a] : mid[a];
+        }
+        nb_begin[c] = off;
+        nb_end[c] = off + cnt;
+        nb_first[c] = -1;
+        nb_nch[c] = 0;
+        // cluster_tree.hpp:96: leaf iff count <= N0 or depth >= 64
+        act_flag[c - next_start] = (cnt > (uint32_t)n0 && child_depth < 64) ? 1 : 0;
+        off += cnt;
+        ++c;
+    }
+}
+
+__global__ void k_compact(int C, int next_start, const int32_t* __restrict__ flag,
+                          const int32_t* __restrict__ pos, int32_t* __restrict__ act) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < C && flag[c]) act[pos[c]] = next_start + c;
+}
+
+__global__ void k_subtree(int v0, int v1, const int32_t* __restrict__ first,
+                          const int32_t* __restrict__ nch, int32_t* __restrict__ size) {
+    const int v = v0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= v1) return;
+    int s = 1;
+    for (int j = 0; j < nch[v]; ++j) s += size[first[v] + j];
+    size[v] = s;
+}
+
+__global__ void k_preorder(int v0, int v1, const int32_t* __restrict__ first,
+                           const int32_t* __restrict__ nch, const int32_t* __restrict__ size,
+                           int32_t* __restrict__ pre) {
+    const int v = v0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= v1) return;
+    if (v == 0) pre[0] = 0;
+    int run = pre[v] + 1;
+    for (int j = 0; j < nch[v]; ++j) {
+        pre[first[v] + j] = run;
+        run += size[first[v] + j];
+    }
+}
+
+__global__ void k_nchunk(int T, const uint32_t* __restrict__ b, const uint32_t* __restrict__ e,
+                         int32_t* __restrict__ nck) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < T) nck[v] = (int32_t)((e[v] - b[v] + kGeomChunk - 1) / kGeomChunk);
+}
+
+__device__ __forceinline__ int find_item(const int32_t* __restrict__ off, int T, int item) {
+    int lo = 0, hi = T - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= item) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Shrink: tight box of each cluster's range (cluster_tree.hpp:88), exact min/max.
+__global__ void __launch_bounds__(256) k_minmax(int T, const int32_t* __restrict__ item_off,
+                                                const uint32_t* __restrict__ nb_begin,
+                                                const uint32_t* __restrict__ nb_end,
+                                                const uint32_t* __restrict__ perm,
+                                                const double* __restrict__ pos,
+                                                unsigned long long* __restrict__ mm) {
+    const int item = blockIdx.x;
+    const int v = find_item(item_off, T, item);
+    const uint32_t b = nb_begin[v] + (uint32_t)(item - item_off[v]) * kGeomChunk;
+    const uint32_t e = min(nb_end[v], b + kGeomChunk);
+    uint64_t lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+    for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
+        const double* p = pos + 3 * (size_t)perm[t];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const uint64_t q = ord_enc(p[a]);
+            lo[a] = q < lo[a] ? q : lo[a];
+            hi[a] = hi[a] < q ? q : hi[a];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = warp_min(lo[a]);
+        hi[a] = warp_max(hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&mm[6 * v + a], (unsigned long long)lo[a]);
+            atomicMax(&mm[6 * v + 3 + a], (unsigned long long)hi[a]);
+        }
+    }
+}
+
+// bbox and centre = (lo + hi) * 0.5 (cluster_tree.hpp:15, 88-89).
+__global__ void k_center(int T, int shrink, const unsigned long long* __restrict__ mm,
+                         const double* __restrict__ nb_box, double* __restrict__ fbox,
+                         double* __restrict__ center) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= T) return;
+    for (int a = 0; a < 3; ++a) {
+        const double lo = shrink ? ord_dec(mm[6 * v + a]) : nb_box[6 * v + a];
+        const double hi = shrink ? ord_dec(mm[6 * v + 3 + a]) : nb_box[6 * v + 3 + a];
+        fbox[6 * v + a] = lo;
+        fbox[6 * v + 3 + a] = hi;
+        center[3 * v + a] = __dmul_rn(__dadd_rn(lo, hi), 0.5);
+    }
+}
+
+// radius^2 = max over the range of norm2(p - c) (cluster_tree.hpp:90-93); non-negative
+// doubles order like their bit patterns, so u64 atomicMax is exact.
+__global__ void __launch_bounds__(256) k_radius(int T, const int32_t* __restrict__ item_off,
+                                                const uint32_t* __restrict__ nb_begin,
+                                                const uint32_t* __restrict__ nb_end,
+                                                const uint32_t* __restrict__ perm,
+                                                const double* __restrict__ pos,
+                                                const double* __restrict__ center,
+                                                unsigned long long* __restrict__ r2max) {
+    const int item = blockIdx.x;
+    const int v = find_item(item_off, T, item);
+    const uint32_t b = nb_begin[v] + (uint32_t)(item - item_off[v]) * kGeomChunk;
+    const uint32_t e = min(nb_end[v], b + kGeomChunk);
+    const double c0 = center[3 * v], c1 = center[3 * v + 1], c2 = center[3 * v + 2];
+    uint64_t m = 0;
+    for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
+        const double* p = pos + 3 * (size_t)perm[t];
+        const double r2 = norm2_rn(__dsub_rn(p[0], c0), __dsub_rn(p[1], c1), __dsub_rn(p[2], c2));
+        const uint64_t q = static_cast<uint64_t>(__double_as_longlong(r2));
+        m = m < q ? q : m;
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(&r2max[v], (unsigned long long)m);
+}
+
+__global__ void k_finalize(int T, int geometry, const int32_t* __restrict__ pre,
+                           const int32_t* __restrict__ size, const uint32_t* __restrict__ nb_begin,
+                           const uint32_t* __restrict__ nb_end, const int32_t* __restrict__ nb_first,
+                           const int32_t* __restrict__ nb_nch, const double* __restrict__ center,
+                           const unsigned long long* __restrict__ r2max, const double* __restrict__ fbox,
+                           double4* __restrict__ geom, int4* __restrict__ info, double* __restrict__ bbox,
+                           int32_t* __restrict__ children, int32_t* __restrict__ nchild) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= T) return;
+    const int p = pre[v];
+    const int nc = nb_nch[v];
+    info[p] = make_int4((int)nb_begin[v], (int)nb_end[v], p + size[v], nc == 0 ? 1 : 0);
+    nchild[p] = nc;
+    for (int j = 0; j < 8; ++j) children[8 * p + j] = j < nc ? pre[nb_first[v] + j] : -1;
+    if (geometry) {
+        const double r = __dsqrt_rn(__longlong_as_double((long long)r2max[v]));
+        geom[p] = make_double4(center[3 * v], center[3 * v + 1], center[3 * v + 2], r);
+        for (int a = 0; a < 6; ++a) bbox[6 * p + a] = fbox[6 * v + a];
+    }
+}
+
+__global__ void k_iota(uint32_t* p, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+
+__global__ void k_zero_hi(unsigned long long* mm, int T) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < T) mm[6 * v + 3] = mm[6 * v + 4] = mm[6 * v + 5] = 0ull;
+}
+
+template <class T>
+void grow(DevArray<T>& a, size_t need, size_t used, cudaStream_t s) {
+    if (a.size() >= need) return;
+    size_t cap = std::max<size_t>(need, a.size() * 2);
+    DevArray<T> b(cap, s);
+    if (used) ST_CUDA(cudaMemcpyAsync(b.get(), a.get(), used * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    a = std::move(b);
+}
+
+inline unsigned blocks(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int32_t read_i32(const int32_t* d, cudaStream_t s) {
+    int32_t h = 0;
+    ST_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+}  // namespace
+
+void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bool geometry,
+                       cudaStream_t s, DevTree& out) {
+    if (n_sz == 0) fail(ST_INVALID_ARGUMENT, "build_tree: empty particle set");
+    if (n0 < 1) fail(ST_INVALID_ARGUMENT, "build_tree: leaf capacity must be >= 1");
+    if (n_sz >= 0x7fffffffull) fail(ST_INVALID_ARGUMENT, "build_tree: more than 2^31-1 particles");
+    const uint32_t n = (uint32_t)n_sz;
+    const int ntiles = (int)blocks(n, kTile);
+
+    // BFS node storage (grown per level)
+    size_t cap = 64;
+    DevArray<uint32_t> nb_begin(cap, s), nb_end(cap, s);
+    DevArray<double> nb_box(6 * cap, s);
+    DevArray<int32_t> nb_first(cap, s), nb_nch(cap, s);
+
+    DevArray<unsigned long long> mm(6, s);
+    {
+        ST_CUDA(cudaMemsetAsync(mm.get(), 0xff, 3 * sizeof(unsigned long long), s));
+        ST_CUDA(cudaMemsetAsync(mm.get() + 3, 0x00, 3 * sizeof(unsigned long long), s));
+        const unsigned g = std::min<unsigned>(blocks(n, 256), 148 * 8);
+        k_tight_all<<<g, 256, 0, s>>>(d_pos, n, mm.get());
+        ST_LAUNCH("k_tight_all");
+        k_root<<<1, 1, 0, s>>>(mm.get(), n, nb_begin.get(), nb_end.get(), nb_box.get());
+        ST_LAUNCH("k_root");
+        count_launch(2);
+    }
+    // root: first/nch = leaf until split
+    ST_CUDA(cudaMemsetAsync(nb_first.get(), 0xff, sizeof(int32_t), s));
+    ST_CUDA(cudaMemsetAsync(nb_nch.get(), 0, sizeof(int32_t), s));
+
+    DevArray<uint32_t> perm(n, s), perm2(n, s);
+    k_iota<<<blocks(n, 256), 256, 0, s>>>(perm.get(), n);  // cluster_tree.hpp:160-161
+    ST_LAUNCH("k_iota");
+    count_launch();
+
+    DevArray<int32_t> seg_of(n, s);
+    DevArray<uint8_t> slot8(n, s);
+    DevArray<uint32_t> blk_cnt((size_t)ntiles * 8, s), blk_off((size_t)(ntiles + 1) * 8, s);
+
+    std::vector<int> level_start{0};
+    int total = 1;
+    int m = n > (uint32_t)n0 ? 1 : 0;
+    DevArray<int32_t> act(std::max(m, 1), s);
+    if (m) ST_CUDA(cudaMemsetAsync(act.get(), 0, sizeof(int32_t), s));
+    int depth = 0;
+
+    while (m > 0) {
+        DevArray<uint32_t> seg_begin(m, s), seg_end(m, s), seg_base((size_t)8 * m, s),
+            seg_cnt((size_t)8 * m, s);
+        DevArray<double> seg_mid((size_t)3 * m, s);
+        DevArray<int32_t> nch(m, s), chbase(m + 1, s);
+
+        k_mkseg<<<blocks(m, 128), 128, 0, s>>>(act.get(), m, nb_begin.get(), nb_end.get(), nb_box.get(),
+                                               seg_begin.get(), seg_end.get(), seg_mid.get());
+        ST_LAUNCH("k_mkseg");
+        k_segof<<<blocks(n, 256), 256, 0, s>>>(n, seg_begin.get(), seg_end.get(), m, seg_of.get());
+        ST_LAUNCH("k_segof");
+        k_slot_hist<<<ntiles, kTileThreads, 0, s>>>(n, d_pos, perm.get(), seg_of.get(), seg_mid.get(),
+                                                    slot8.get(), blk_cnt.get());
+        ST_LAUNCH("k_slot_hist");
+        launch_scan_cols(blk_cnt.get(), blk_off.get(), ntiles, 8, s);
+        k_segbase<<<blocks((size_t)2 * m * 32, 256), 256, 0, s>>>(m, seg_begin.get(), seg_end.get(),
+                                                                  slot8.get(), blk_off.get(),
+                                                                  seg_base.get(), seg_cnt.get());
+        ST_LAUNCH("k_segbase");
+        k_scatter<<<ntiles, kTileThreads, 0, s>>>(n, slot8.get(), seg_of.get(), blk_off.get(),
+                                                  seg_begin.get(), seg_base.get(), seg_cnt.get(),
+                                                  perm.get(), perm2.get());
+        ST_LAUNCH("k_scatter");
+        perm.swap(perm2);
+        k_nch<<<blocks(m, 128), 128, 0, s>>>(m, seg_cnt.get(), nch.get());
+        ST_LAUNCH("k_nch");
+        launch_scan_i32(nch.get(), chbase.get(), m, s);
+        count_launch(6);
+        const int C = read_i32(chbase.get() + m, s);
+
+        const size_t need = (size_t)total + C;
+        grow(nb_begin, need, total, s);
+        grow(nb_end, need, total, s);
+        grow(nb_first, need, total, s);
+        grow(nb_nch, need, total, s);
+        grow(nb_box, 6 * need, 6 * (size_t)total, s);
+
+        DevArray<int32_t> flag(C, s), fpos(C + 1, s);
+        k_children<<<blocks(m, 128), 128, 0, s>>>(m, act.get(), seg_begin.get(), seg_cnt.get(),
+                                                  chbase.get(), total, n0, depth + 1, nb_box.get(),
+                                                  nb_box.get(), nb_begin.get(), nb_end.get(),
+                                                  nb_first.get(), nb_nch.get(), flag.get());
+        ST_LAUNCH("k_children");
+        launch_scan_i32(flag.get(), fpos.get(), C, s);
+        count_launch();
+        const int m2 = read_i32(fpos.get() + C, s);
+        DevArray<int32_t> act2(std::max(m2, 1), s);
+        if (m2) {
+            k_compact<<<blocks(C, 256), 256, 0, s>>>(C, total, flag.get(), fpos.get(), act2.get());
+            ST_LAUNCH("k_compact");
+            count_launch();
+        }
+        act = std::move(act2);
+        level_start.push_back(total);
+        total += C;
+        m = m2;
+        ++depth;
+    }
+    level_start.push_back(total);
+    const int T = total;
+    const int L = (int)level_start.size() - 1;
+
+    DevArray<int32_t> size(T, s), pre(T, s);
+    for (int d = L - 1; d >= 0; --d) {
+        const int v0 = level_start[d], v1 = level_start[d + 1];
+        k_subtree<<<blocks(v1 - v0, 128), 128, 0, s>>>(v0, v1, nb_first.get(), nb_nch.get(), size.get());
+        ST_LAUNCH("k_subtree");
+        count_launch();
+    }
+    for (int d = 0; d < L; ++d) {
+        const int v0 = level_start[d], v1 = level_start[d + 1];
+        k_preorder<<<blocks(v1 - v0, 128), 128, 0, s>>>(v0, v1, nb_first.get(), nb_nch.get(), size.get(),
+                                                         pre.get());
+        ST_LAUNCH("k_preorder");
+        count_launch();
+    }
+
+    out.n = n;
+    out.ncl = T;
+    out.depth = L - 1;
+    out.geom.alloc(geometry ? T : 0, s);
+    out.bbox.alloc(geometry ? 6 * (size_t)T : 0, s);
+    out.info.alloc(T, s);
+    out.children.alloc(8 * (size_t)T, s);
+    out.nchild.alloc(T, s);
+
+    DevArray<double> center, fbox;
+    DevArray<unsigned long long> r2max;
+    if (geometry) {
+        DevArray<int32_t> nck(T, s), ioff(T + 1, s);
+        k_nchunk<<<blocks(T, 256), 256, 0, s>>>(T, nb_begin.get(), nb_end.get(), nck.get());
+        ST_LAUNCH("k_nchunk");
+        launch_scan_i32(nck.get(), ioff.get(), T, s);
+        count_launch();
+        const int items = read_i32(ioff.get() + T, s);
+        center.alloc(3 * (size_t)T, s);
+        fbox.alloc(6 * (size_t)T, s);
+        r2max.alloc(T, s);
+        r2max.zero();
+        DevArray<unsigned long long> nmm;
+        if (shrink) {
+            nmm.alloc(6 * (size_t)T, s);
+            // lo slots = +inf ordering (all ones), hi slots = 0
+            nmm.fill_bytes(0xff);
+            k_zero_hi<<<blocks(T, 256), 256, 0, s>>>(nmm.get(), T);
+            ST_LAUNCH("k_zero_hi");
+            k_minmax<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), perm.get(), d_pos,
+                                           nmm.get());
+            ST_LAUNCH("k_minmax");
+            count_launch(2);
+        }
+        k_center<<<blocks(T, 128), 128, 0, s>>>(T, shrink ? 1 : 0, nmm.get(), nb_box.get(), fbox.get(),
+                                                center.get());
+        ST_LAUNCH("k_center");
+        k_radius<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), perm.get(), d_pos,
+                                       center.get(), r2max.get());
+        ST_LAUNCH("k_radius");
+        count_launch(2);
+    }
+    k_finalize<<<blocks(T, 128), 128, 0, s>>>(T, geometry ? 1 : 0, pre.get(), size.get(), nb_begin.get(),
+                                              nb_end.get(), nb_first.get(), nb_nch.get(), center.get(),
+                                              r2max.get(), fbox.get(), out.geom.get(), out.info.get(),
+                                              out.bbox.get(), out.children.get(), out.nchild.get());
+    ST_LAUNCH("k_finalize");
+    count_launch();
+    out.perm = std::move(perm);
+}
+
+}  // namespace st

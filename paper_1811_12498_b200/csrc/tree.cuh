@@ -1,0 +1,28 @@
+// K1: device octree build, bit-exact with build_tree (cluster_tree.hpp:152-192).
+#pragma once
+
+#include <vector>
+
+#include "st_common.cuh"
+
+namespace st {
+
+// Cluster tree in pre-order (id 0 = root), device resident.
+struct DevTree {
+    size_t n = 0;
+    int ncl = 0;
+    int depth = 0;
+    DevArray<double4> geom;      // center xyz, radius
+    DevArray<int4> info;         // begin, end, next (pre-order id after the subtree), is_leaf
+    DevArray<double> bbox;       // lo xyz, hi xyz per cluster
+    DevArray<int32_t> children;  // 8 per cluster, pre-order ids, -1 padded
+    DevArray<int32_t> nchild;    // n_children
+    DevArray<uint32_t> perm;     // tree index -> original index (to_original)
+};
+
+// Builds the tree of n points (xyz interleaved, device) with leaf capacity n0.
+// geometry=false skips bbox/center/radius (used for the target ordering tree).
+void build_tree_device(const double* d_pos, size_t n, int n0, bool shrink, bool geometry,
+                       cudaStream_t s, DevTree& out);
+
+}  // namespace st

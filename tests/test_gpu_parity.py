@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference compiled in
+place (oracle/_ref) and the C restatement (oracle/liboracle.so).
+
+Bars (BASELINE.json north_star): tree and interaction lists bit-exact;
+velocities within 1e-12 relative L2 of the reference treecode; error against
+direct summation equal to the reference's within 1%."""
+import numpy as np
+import pytest
+
+from conftest import as_dict
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-12  # north_star: fp64 velocities within 1e-12 relative L2 of the reference treecode
+
+
+def tree_equal(T_gpu, T_ref):
+    assert T_gpu.ncl == T_ref.ncl
+    assert np.array_equal(T_gpu.to_original, T_ref.to_original)
+    assert np.array_equal(T_gpu.begin, T_ref.begin) and np.array_equal(T_gpu.end, T_ref.end)
+    assert np.array_equal(T_gpu.children, T_ref.children)
+    assert np.array_equal(T_gpu.n_children, T_ref.n_children)
+    assert np.array_equal(T_gpu.is_leaf, T_ref.is_leaf)
+    # centre, radius and bbox bytes (cluster_tree.hpp:88-93)
+    assert np.array_equal(T_gpu.geom.view(np.uint64), T_ref.geom.view(np.uint64))
+
+
+@pytest.mark.parametrize("kind,n,n0,shrink", [
+    ("cube", 10000, 500, True), ("cube", 10000, 500, False), ("unit", 3000, 1, True),
+    ("sphere", 20000, 200, True), ("sphere", 20000, 200, False), ("mixture", 50000, 100, True),
+    ("cube", 200000, 2000, True), ("unit", 7, 1, True),
+])
+def test_tree_bit_exact(S, need_ref, kind, n, n0, shrink):
+    ps = S.generate(kind, n, 12345, True)
+    T = S.build_tree(ps, n0, shrink)
+    ctx = need_ref.RefContext(as_dict(ps), 0, 0.5, n0, shrink)
+    tree_equal(T, ctx.tree())
+
+
+def test_tree_corner_cases(S, need_ref):
+    # eight cube corners with unit leaves (test_cluster_tree.cpp:63-83)
+    pos = np.array([[x, y, z] for z in (0.0, 1.0) for y in (0.0, 1.0) for x in (0.0, 1.0)])
+    ps = S.ParticleSet(pos, np.tile([1.0, 0, 0], (8, 1)))
+    T = S.build_tree(ps, 1, True)
+    assert T.ncl == 9 and T.n_children[0] == 8 and T.is_leaf.sum() == 8
+    assert np.all(T.radius[T.is_leaf == 1] == 0.0)
+    ctx = need_ref.RefContext(dict(position=pos, force_weight=ps.force_weight), 0, 0.5, 1, True,
+                              sto=True, stre=False)
+    tree_equal(T, ctx.tree())
+    # single particle (:52-61)
+    one = S.ParticleSet(np.array([[0.3, -0.2, 0.9]]), np.array([[1.0, 0, 0]]))
+    T1 = S.build_tree(one, 2000, False)
+    assert T1.ncl == 1 and T1.is_leaf[0] == 1 and T1.radius[0] == 0.0
+    assert np.array_equal(T1.center[0], one.position[0])
+
+
+def test_moments_match_reference(S, need_ref):
+    ps = S.generate("cube", 20000, 7, True)
+    T = S.build_tree(ps, 300, True)
+    for p in (0, 3, 8):
+        m = S.compute_moments(T, p, S.KernelSelection.both())
+        ctx = need_ref.RefContext(as_dict(ps), p, 0.5, 300, True)
+        r = ctx.moments()
+        for key, mine in (("stok", m.stok), ("str", m.str), ("trace", m.trace), ("sym", m.sym)):
+            ref = r[key].reshape(mine.shape)
+            scale = np.abs(ref).max(axis=(1, 2), keepdims=True) + 1e-300
+            assert np.max(np.abs(mine - ref) / scale) < 1e-13, (p, key)
+
+
+def test_direct_matches_reference(S, need_ref):
+    ps = S.generate("cube", 3000, 99, True)
+    for sel in (S.KernelSelection.both(), S.KernelSelection.stokeslet_only(),
+                S.KernelSelection.stresslet_only()):
+        u = S.contracted_direct_velocity(ps, sel)
+        ref = need_ref.ref_direct_at(as_dict(ps), np.arange(3000), sel.stokeslet_enabled, sel.stresslet_enabled)
+        assert S.relative_error(ref, u) < 1e-14
+    sub = S.contracted_direct_velocity(ps, S.KernelSelection.both(), 10, 25)
+    full = S.contracted_direct_velocity(ps, S.KernelSelection.both())
+    assert np.array_equal(sub, full[10:25])
+    assert S.contracted_direct_velocity(ps, S.KernelSelection.both(), 5, 5).shape == (0, 3)
+    at = S.contracted_direct_velocity_at(ps, S.KernelSelection.both(), [7, 3, 2999])
+    assert np.array_equal(at, full[[7, 3, 2999]])
+
+
+def test_naive_matches_contracted(S):
+    # contracted == naive at <= 1e-13 (test_kernels.cpp:158-175)
+    for n in (2, 10, 500):
+        ps = S.generate("unit", n, 100 + n, True)
+        for sel in (S.KernelSelection.both(), S.KernelSelection.stokeslet_only(),
+                    S.KernelSelection.stresslet_only()):
+            a = S.naive_direct_velocity(ps, sel)
+            b = S.contracted_direct_velocity(ps, sel)
+            num = np.linalg.norm(a - b, axis=1)
+            den = np.maximum(np.linalg.norm(a, axis=1), np.linalg.norm(b, axis=1))
+            assert np.all(num <= 1e-13 * np.maximum(den, 1e-300))
+
+
+def test_naive_hand_cases(S):
+    # test_kernels.cpp:130-156
+    ps = S.ParticleSet(np.array([[0, 0, 0], [1, 0, 0.0]]), np.array([[1, 0, 0], [1, 0, 0.0]]))
+    u = S.naive_direct_velocity(ps, S.KernelSelection.stokeslet_only())
+    assert np.array_equal(u, [[2, 0, 0], [2, 0, 0]])
+    ps = S.ParticleSet(np.array([[0, 0, 0], [1, 0, 0.0]]), np.zeros((2, 3)), np.array([[1, 0, 0], [1, 0, 0.0]]),
+                       np.array([[1, 0, 0], [1, 0, 0.0]]))
+    u = S.naive_direct_velocity(ps, S.KernelSelection.stresslet_only())
+    assert np.array_equal(u, [[-1, 0, 0], [1, 0, 0]])
+
+
+def test_coincident_points_raise_domain_error(S):
+    # test_kernels.cpp:188-196
+    ps = S.ParticleSet(np.array([[0, 0, 0], [1, 1, 1], [0, 0, 0.0]]), np.tile([1.0, 0, 0], (3, 1)))
+    with pytest.raises(S.DomainError):
+        S.contracted_direct_velocity(ps, S.KernelSelection.stokeslet_only())
+    with pytest.raises(S.DomainError):
+        S.naive_direct_velocity(ps, S.KernelSelection.stokeslet_only())
+    with pytest.raises(S.DomainError):
+        S.treecode_velocity(ps, S.TreecodeParams(kernels=S.KernelSelection.stokeslet_only()))
+
+
+def random_cluster(S, rng, n, p):
+    ps = S.generate("unit", n, int(rng.integers(1 << 30)), True)
+    T = S.build_tree(ps, n + 1, True)
+    return ps, T
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 4, 6, 8, 10, 12, 16])
+def test_farfield_pairs_match_reference(S, need_ref, p):
+    rng = np.random.default_rng(p)
+    dxs, stoks, strs, refs = [], [], [], []
+    for pair in range(24):
+        ps, T = random_cluster(S, rng, 20 + pair, p)
+        m = S.compute_moments(T, p, S.KernelSelection.both())
+        d = rng.normal(size=3)
+        d *= T.radius[0] * (1.5 + 2.5 * rng.uniform()) / np.linalg.norm(d)
+        stok, strm, tr, sy = m.stok[0], m.str[0], m.trace[0], m.sym[0]
+        refs.append(need_ref.ref_farfield_pair(d, p, stok, strm, tr, sy))
+        dxs.append(d)
+        stoks.append(stok)
+        strs.append(strm)
+    u = S.farfield_pairs(np.array(dxs), p, np.array(stoks), np.array(strs))
+    ref = np.array(refs)
+    rel = np.linalg.norm(u - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert rel.max() < 1e-12, rel.max()
+
+
+def test_coulomb_matches_reference(S, need_ref):
+    rng = np.random.default_rng(3)
+    dx = rng.normal(size=(50, 3))
+    for pmax in (0, 3, 10):
+        b = S.coulomb_coeffs(dx, pmax)
+        for i in range(0, 50, 7):
+            ref = need_ref.ref_coulomb(dx[i], pmax)[:-1]
+            assert np.max(np.abs(b[i] - ref) / np.abs(ref).max()) < 1e-13
+    # hand values (test_coulomb.cpp:11-25)
+    b = S.coulomb_coeffs([[1, 0, 0], [0, 2, 0]], 3)
+    assert b[0][0] == 1.0 and b[0][1 + 2] == 1.0  # b^0, b^(1,0,0)
+    with pytest.raises(S.DomainError):
+        S.coulomb_coeffs([[0, 0, 0]], 2)
+
+
+def run_pair(S, O, ps, order, theta, n0, shrink=True, sel=None):
+    sel = sel or S.KernelSelection.both()
+    prm = S.TreecodeParams(order=order, theta=theta, leaf_capacity=n0, shrink=shrink, kernels=sel)
+    res = S.treecode_velocity(ps, prm, per_target=True)
+    ctx = O.RefContext(as_dict(ps), order, theta, n0, shrink, sel.stokeslet_enabled, sel.stresslet_enabled)
+    u_ref, pt_ref, st_ref = ctx.eval(src_idx=np.arange(ps.size()), threads=8)
+    return res, u_ref, pt_ref, st_ref
+
+
+@pytest.mark.parametrize("order,theta,n0", [(6, 0.5, 500), (2, 0.7, 200), (10, 0.5, 1000), (0, 0.3, 64)])
+def test_treecode_cfg0_parity(S, need_ref, order, theta, n0):
+    # BASELINE.json configs[0]: N = 10,000 cube, theta 0.5, p 6, N0 500
+    ps = S.generate("cube", 10000, 12345, True)
+    res, u_ref, pt_ref, st_ref = run_pair(S, need_ref, ps, order, theta, n0)
+    # interaction lists: per-target (visited, accepted, direct pairs) bit-exact
+    assert np.array_equal(res.per_target, pt_ref)
+    assert res.stats.farfield_evals == st_ref["farfield_evals"]
+    assert res.stats.direct_pairs == st_ref["direct_pairs"]
+    assert res.stats.clusters_visited == st_ref["clusters_visited"]
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_treecode_error_vs_direct_matches_reference(S, need_ref):
+    ps = S.generate("cube", 10000, 12345, True)
+    res, u_ref, _, _ = run_pair(S, need_ref, ps, 6, 0.5, 500)
+    direct = S.contracted_direct_velocity(ps, S.KernelSelection.both())
+    e_gpu = S.relative_error(direct, res.velocity)
+    e_ref = S.relative_error(direct, u_ref)
+    assert abs(e_gpu - e_ref) <= 0.01 * e_ref
+
+
+@pytest.mark.parametrize("sel", ["stokeslet_only", "stresslet_only"])
+def test_treecode_kernel_selection(S, need_ref, sel):
+    k = getattr(S.KernelSelection, sel)()
+    ps = S.generate("cube", 8000, 77, True)
+    res, u_ref, pt_ref, _ = run_pair(S, need_ref, ps, 5, 0.6, 300, sel=k)
+    assert np.array_equal(res.per_target, pt_ref)
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_treecode_sphere_and_mixture(S, need_ref):
+    for kind, order, theta, n0 in (("sphere", 10, 0.7, 500), ("mixture", 8, 0.6, 300)):
+        ps = S.generate(kind, 30000, 12345, True)
+        res, u_ref, pt_ref, _ = run_pair(S, need_ref, ps, order, theta, n0)
+        assert np.array_equal(res.per_target, pt_ref)
+        assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_disjoint_targets(S, need_ref):
+    # configs[4] shape, small: mixture sources, uniform disjoint targets
+    ps = S.generate("mixture", 20000, 12345, True)
+    tg = S.generate("points", 5000, 67890).position
+    prm = S.TreecodeParams(order=8, theta=0.6, leaf_capacity=300)
+    res = S.treecode_velocity_targets(ps, tg, prm, per_target=True)
+    ctx = need_ref.RefContext(as_dict(ps), 8, 0.6, 300, True)
+    u_ref, pt_ref, _ = ctx.eval(xyz=tg, threads=8)
+    assert np.array_equal(res.per_target, pt_ref)
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_vanishing_theta_is_direct(S):
+    # test_engine.cpp:12-24
+    ps = S.generate("unit", 3000, 9001, True)
+    res = S.treecode_velocity(ps, S.TreecodeParams(order=5, theta=1e-9, leaf_capacity=100))
+    direct = S.contracted_direct_velocity(ps, S.KernelSelection.both())
+    assert res.stats.farfield_evals == 0
+    assert S.relative_error(direct, res.velocity) <= 1e-13
+
+
+def test_single_leaf_equals_direct(S):
+    # test_engine.cpp:26-36 (bit-for-bit in the reference; same formula order here up to FMA)
+    ps = S.generate("unit", 150, 404, True)
+    res = S.treecode_velocity(ps, S.TreecodeParams(order=2, theta=0.5, leaf_capacity=2000))
+    direct = S.contracted_direct_velocity(ps, S.KernelSelection.both())
+    assert S.relative_error(direct, res.velocity) <= 1e-15
+    assert res.stats.farfield_evals == 0
+
+
+def test_single_particle_zero_velocity(S):
+    ps = S.ParticleSet(np.array([[1.0, 2, 3]]), np.array([[4.0, 5, 6]]))
+    res = S.treecode_velocity(ps, S.TreecodeParams(kernels=S.KernelSelection.stokeslet_only()))
+    assert np.array_equal(res.velocity, [[0.0, 0, 0]])
+
+
+def test_determinism_across_runs(S):
+    ps = S.generate("cube", 50000, 5, True)
+    prm = S.TreecodeParams(order=4, theta=0.5, leaf_capacity=400)
+    a = S.treecode_velocity(ps, prm).velocity
+    b = S.parallel_velocity(ps, S.TreecodeParams(order=4, theta=0.5, leaf_capacity=400, workers=4)).velocity
+    assert a.tobytes() == b.tobytes()
+
+
+def test_validation_errors(S):
+    ps = S.generate("cube", 100, 1, True)
+    bad = S.ParticleSet(ps.position.copy(), ps.force_weight, ps.dipole_weight, ps.normal.copy())
+    bad.normal[17] *= 1.0 + 1e-9
+    with pytest.raises(S.InvalidArgument, match="normal 17 is not unit length"):
+        S.treecode_velocity(bad, S.TreecodeParams())
+    bad2 = S.ParticleSet(ps.position.copy(), ps.force_weight)
+    bad2.position[3, 1] = np.nan
+    with pytest.raises(S.InvalidArgument, match="position"):
+        S.treecode_velocity(bad2, S.TreecodeParams(kernels=S.KernelSelection.stokeslet_only()))
+    with pytest.raises(S.InvalidArgument):
+        S.treecode_velocity(S.ParticleSet(np.zeros((0, 3))), S.TreecodeParams())
