@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the treecode evaluation hot path (BASELINE.json metric).
+
+One step = one full treecode evaluation (tree build -> moments -> far field ->
+near field -> velocities in original order) of BASELINE.json configs[1]
+(N = 1,000,000 uniform-cube particles, theta 0.5, p 8, N0 2000, Stokeslet +
+stresslet, targets = sources) unless --config says otherwise.
+
+value : target velocities/s, whole job, inputs resident in HBM, device time
+        (CUDA events on the launching stream), max over ranks.
+e2e   : the same metric through the public C ABI with pinned HOST buffers:
+        H2D of the particle arrays, the treecode, D2H of the velocities.
+With torchrun (N > 1) every rank rebuilds the tree and moments (bit-identical)
+and evaluates its work-balanced shard of the Morton-ordered target batches;
+the velocities are combined with one NCCL collective.
+
+--impl reference runs the reference's own CPU treecode (the headers under
+/root/reference compiled in place, oracle/_ref/libstref.so) on the host cores.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    "cfg0": dict(kind="cube", n=10_000, order=6, theta=0.5, n0=500, targets=None,
+                 desc="cfg0: N=10,000 uniform cube [-0.5,0.5)^3, theta=0.5, p=6, N0=500"),
+    "cfg1": dict(kind="cube", n=1_000_000, order=8, theta=0.5, n0=2000, targets=None,
+                 desc="cfg1: N=1,000,000 uniform cube [-0.5,0.5)^3, theta=0.5, p=8, N0=2000"),
+    "cfg2": dict(kind="sphere", n=4_000_000, order=10, theta=0.7, n0=2000, targets=None,
+                 desc="cfg2: N=4,000,000 uniform on the unit sphere, nu = normal, theta=0.7, p=10, N0=2000"),
+    "cfg3": dict(kind="cube", n=16_000_000, order=8, theta=0.5, n0=4000, targets=None,
+                 desc="cfg3: N=16,000,000 uniform cube, theta=0.5, p=8, N0=4000"),
+    "cfg4": dict(kind="mixture", n=8_000_000, order=8, theta=0.6, n0=2000, targets=8_000_000,
+                 desc="cfg4: 8M sources from 16 Gaussians (sigma 0.05) / 8M uniform disjoint targets, "
+                      "theta=0.6, p=8, N0=2000"),
+}
+SRC_SEED, TGT_SEED = 12345, 67890
+METRIC = "target velocities/s"
+F_NEAR = 48  # reference-algorithmic flops per direct pair, both kernels
+
+
+def f_far(p):
+    """Reference-algorithmic flops per accepted particle-cluster pair."""
+    E = lambda n: (n + 1) * (n + 2) * (n + 3) // 6
+    P = p + 2
+    return (11 * E(P) + 5 * P - 16) + 41 * E(p) + (147 * E(p) + 3) + 6
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(cfg):
+    import paper_1811_12498_b200 as S
+    ps = S.generate(cfg["kind"], cfg["n"], SRC_SEED, True)
+    tg = S.generate("points", cfg["targets"], TGT_SEED).position if cfg["targets"] else None
+    return ps, tg
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def cpu_reference_step(ps, tg, cfg, threads, sample):
+    """Reference CPU treecode (oracle/_ref) on a bounded sample: build + moments in full,
+    traversal of `sample` strided targets on `threads` threads, extrapolated to all N
+    targets (the reference's own --direct-sample idiom, bench.hpp:247-248)."""
+    from oracle import oracle as O
+    d = dict(position=ps.position, force_weight=ps.force_weight, dipole_weight=ps.dipole_weight,
+             normal=ps.normal)
+    t0 = time.perf_counter()
+    ctx = O.RefContext(d, cfg["order"], cfg["theta"], cfg["n0"], True, True, True, workers=threads)
+    t1 = time.perf_counter()
+    nt = cfg["targets"] or cfg["n"]
+    stride = max(1, nt // sample)
+    idx = np.arange(0, nt, stride)[:sample]
+    t2 = time.perf_counter()
+    if tg is None:
+        ctx.eval(src_idx=idx, threads=threads)
+    else:
+        ctx.eval(xyz=tg[idx], threads=threads)
+    t3 = time.perf_counter()
+    ctx.close()
+    full = (t1 - t0) + (t3 - t2) * nt / len(idx)
+    return nt / full, dict(build_moments_s=t1 - t0, sample_targets=len(idx), sample_traverse_s=t3 - t2)
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if not O.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstref.so not built"}))
+        return
+    threads = os.cpu_count() or 1
+    ps, tg = make_inputs(cfg)
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_reference_step(ps, tg, cfg, threads, max(64, sample // 8))
+    vals = []
+    info = None
+    for _ in range(args.steps):
+        v, info = cpu_reference_step(ps, tg, cfg, threads, sample)
+        vals.append(v)
+    value = float(np.mean(vals))
+    nt = cfg["targets"] or cfg["n"]
+    desc = (f"reference CPU treecode (headers compiled in place), {threads} threads: full build + moments, "
+            f"traversal of {info['sample_targets']} strided targets extrapolated to {nt}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "targets/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": nt / value * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
+        "config": config_block(cfg, args),
+        "cpu_baseline": {"value": value, "unit": "targets/s", "cores": threads, "kind": "reference",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "targets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": info,
+    }
+    print(json.dumps(line))
+
+
+def config_block(cfg, args):
+    return {"workload": cfg["desc"], "n_sources": cfg["n"], "n_targets": cfg["targets"] or cfg["n"],
+            "order": cfg["order"], "theta": cfg["theta"], "leaf_capacity": cfg["n0"], "shrink": True,
+            "kernels": "stokeslet+stresslet", "seeds": [SRC_SEED, TGT_SEED] if cfg["targets"] else [SRC_SEED],
+            "l2": "flushed between timed steps (512 MiB write, outside the step events)",
+            "parallelism": f"targets sharded over {int(os.environ.get('WORLD_SIZE', '1'))} GPU(s), "
+                           "tree+moments replicated"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_12498_b200 as S
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    # inputs: generated on rank 0 host, broadcast over NCCL (replicated sources)
+    nt = cfg["targets"] or cfg["n"]
+    n = cfg["n"]
+    if rank == 0:
+        ps, tg = make_inputs(cfg)
+        host = np.concatenate([ps.position, ps.force_weight, ps.dipole_weight, ps.normal], axis=0)
+    else:
+        ps, tg, host = None, None, None
+    dsrc = torch.empty((4 * n, 3), dtype=torch.float64, device=dev)
+    dtg = torch.empty((nt, 3), dtype=torch.float64, device=dev) if cfg["targets"] else None
+    if rank == 0:
+        dsrc.copy_(torch.from_numpy(host))
+        if dtg is not None:
+            dtg.copy_(torch.from_numpy(tg))
+    if world > 1:
+        dist.broadcast(dsrc, 0)
+        if dtg is not None:
+            dist.broadcast(dtg, 0)
+    dout = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    prm = S.TreecodeParams(order=cfg["order"], theta=cfg["theta"], leaf_capacity=cfg["n0"], shrink=True)
+    base = dsrc.data_ptr()
+    stride = n * 3 * 8
+    ptrs = (base, base + stride, base + 2 * stride, base + 3 * stride)
+
+    def step():
+        dout.zero_()
+        r = S.treecode_velocity_device(*ptrs, n, prm, dout.data_ptr(),
+                                       targets_ptr=None if dtg is None else dtg.data_ptr(),
+                                       n_targets=nt if dtg is not None else 0, shard=rank, n_shards=world,
+                                       stream=sptr)
+        if world > 1:
+            dist.all_reduce(dout)  # disjoint shards: x + 0 + ... + 0 is exact
+        return r
+
+    peak = S.fp64_peak(0.3)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    near_t = far_t = 0.0
+    stats = None
+    launches = 0
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ev[k][0].record(stream)
+            r = step()
+            ev[k][1].record(stream)
+            near_t += r.time_near_s
+            far_t += r.time_far_s
+            launches += r.gpu_launches
+            stats = r.stats
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    t = torch.tensor([tot_ms, near_t, far_t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms, near_max, far_max = t.tolist()
+    value = nt * args.steps / (tot_ms * 1e-3)
+
+    # ---- e2e through the public C ABI with pinned host buffers (H2D + treecode + D2H)
+    e2e = None
+    hsrc = torch.empty((4 * n, 3), dtype=torch.float64).pin_memory()
+    hout = torch.empty((nt, 3), dtype=torch.float64).pin_memory()
+    htg = torch.empty((nt, 3), dtype=torch.float64).pin_memory() if dtg is not None else None
+    if rank == 0:
+        hsrc.copy_(torch.from_numpy(host))
+        if htg is not None:
+            htg.copy_(torch.from_numpy(tg))
+    h2d_bytes = hsrc.numel() * 8 + (htg.numel() * 8 if htg is not None else 0)
+    d2h_bytes = hout.numel() * 8
+
+    def e2e_step():
+        if rank == 0:
+            dsrc.copy_(hsrc, non_blocking=True)
+            if dtg is not None:
+                dtg.copy_(htg, non_blocking=True)
+        if world > 1:
+            dist.broadcast(dsrc, 0)
+            if dtg is not None:
+                dist.broadcast(dtg, 0)
+        step()
+        if rank == 0:
+            hout.copy_(dout, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ee[k][0].record(stream)
+        e2e_step()
+        ee[k][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ee)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_val = nt * args.steps / (e2e_ms.item() * 1e-3)
+    if rank == 0:
+        u_e2e = hout.numpy().copy()
+        assert np.isfinite(u_e2e).all()
+    e2e = {"value": e2e_val, "unit": "targets/s", "h2d_bytes_per_step": int(h2d_bytes) if rank == 0 else 0,
+           "d2h_bytes_per_step": int(d2h_bytes), "path": "st_treecode_velocity_device on pinned-host copies"}
+
+    # ---- roofline of the dominant kernel (near field), reference-algorithmic flops
+    near_flops = F_NEAR * stats.direct_pairs
+    far_flops = f_far(cfg["order"]) * stats.farfield_evals
+    near_s = near_max / args.steps
+    far_s = far_max / args.steps
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get("near_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    ach_near = near_flops / near_s * 1e-12 if world == 1 else None
+    ach_far = far_flops / far_s * 1e-12 if world == 1 else None
+    roof = {"bound": "fp64", "kernel": "k_near (near-field leaf direct sum)",
+            "achieved": ach_near, "peak": peak, "unit": "TFLOP/s",
+            "frac": (ach_near / peak) if ach_near else None, "traffic": traffic,
+            "flops_per_launch": near_flops, "flop_convention": "reference-algorithmic, 48 flop per direct pair",
+            "peak_source": "live DFMA-loop probe in this run (MEASURED_PEAKS.json has no FP64 figure)",
+            "far": {"kernel": "k_far (MAC traversal + Taylor far field)", "achieved": ach_far,
+                    "frac": (ach_far / peak) if ach_far else None, "flops_per_launch": far_flops,
+                    "flop_convention": f"reference-algorithmic (reference-equivalent), {f_far(cfg['order'])} "
+                                       "flop per accepted pair; executed flops are ~15x fewer (harmonic "
+                                       "4-potential form, DESIGN.md)"},
+            "near_s": near_s, "far_s": far_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            if O.have_ref():
+                threads = os.cpu_count() or 1
+                v, info = cpu_reference_step(ps, tg, cfg, threads, args.ref_sample)
+                cpu = {"value": v, "unit": "targets/s", "cores": threads, "kind": "reference",
+                       "sample": f"reference treecode compiled in place, full build+moments, "
+                                 f"{info['sample_targets']} strided targets traversed on {threads} threads, "
+                                 f"extrapolated to {nt} targets ({info})"}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "targets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
+            "config": config_block(cfg, args), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "cpu_baseline": cpu, "clocks": clocks.summary(),
+            "stats": {"farfield_evals": stats.farfield_evals, "direct_pairs": stats.direct_pairs,
+                      "clusters_visited": stats.clusters_visited},
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
+    ap.add_argument("--ref-sample", type=int, default=4000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()
