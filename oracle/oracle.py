@@ -91,6 +91,8 @@ def _load_or():
         L.or_direct_at.argtypes = [_sz, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _i64p, _sz, C.c_int, _dp]
         L.or_direct_points.argtypes = [_sz, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _dp, _sz, _dp]
         L.or_relative_error.argtypes = [_sz, _dp, _dp, C.POINTER(C.c_double)]
+        L.or_mac.argtypes = [C.c_double, C.c_double, C.c_double]
+        L.or_mac.restype = C.c_int
         _or = L
     return _or
 
@@ -281,6 +283,10 @@ def or_direct_points(ps, xyz, sto=True, stre=True):
     _check(L.or_direct_points(n, p[0], p[1], p[2], p[3], int(sto), int(stre), xyz.reshape(-1), len(xyz),
                               u.reshape(-1)), "or_direct_points")
     return u
+
+
+def or_mac(radius, dist2, theta) -> bool:
+    return bool(_load_or().or_mac(radius, dist2, theta))
 
 
 def relative_error(u_ref, u_test) -> float:

@@ -739,3 +739,9 @@ int or_relative_error(size_t n, const double *ref, const double *test, double *o
     *out = sqrt(num / den);
     return OR_OK;
 }
+
+/* mac (cluster_tree.hpp:47-50): accept iff dist2 != 0 and r*r <= theta*theta*dist2 */
+int or_mac(double radius, double dist2, double theta) {
+    if (dist2 == 0.0) return 0;
+    return radius * radius <= theta * theta * dist2;
+}

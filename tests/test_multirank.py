@@ -1,0 +1,79 @@
+"""CPU, world_size 2 over gloo: the N > 1 plumbing of bench.py / DESIGN.md "Multi-GPU".
+
+Every rank derives the same work-balanced cut of the Morton-ordered 32-target
+batches (no communication), owns a disjoint shard, and the velocity buffers are
+combined by one collective.  Because the shards are disjoint, x + 0 is exact and
+the combined result is bit-identical to the single-rank result.  The per-target
+velocities here come from the oracle (no GPU in this container); the CUDA path
+writes the same disjoint-shard layout."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1811_12498_b200 as S
+    from oracle import oracle as O
+    ps = S.generate("cube", 3000, 12345, True)
+    d = dict(position=ps.position, force_weight=ps.force_weight, dipole_weight=ps.dipole_weight,
+             normal=ps.normal)
+    # replicated sources: rank 0's copy broadcast to everyone
+    src = torch.from_numpy(ps.position.copy()) if rank == 0 else torch.zeros((3000, 3), dtype=torch.float64)
+    dist.broadcast(src, 0)
+    assert np.array_equal(src.numpy(), ps.position)
+    # batch order = leaf-capacity-32 octree over the targets (same recipe as the CUDA path)
+    order = O.or_build_tree(d, 32, False).to_original.astype(np.int64)
+    nwarps = (len(order) + 31) // 32
+    u_all, _, pt = O.or_treecode(d, 4, 0.5, 200, per_target=True, threads=2)
+    # per-warp cost from the exact per-target counts; identical on every rank
+    cost = np.zeros(nwarps)
+    for w in range(nwarps):
+        tg = order[32 * w:32 * (w + 1)]
+        cost[w] = pt[tg, 1].sum() * 100 + pt[tg, 2].sum()
+    cuts = S.shard_cuts(cost, world)
+    mine = order[32 * cuts[rank]:32 * cuts[rank + 1]]
+    out = torch.zeros((3000, 3), dtype=torch.float64)
+    out[torch.from_numpy(mine)] = torch.from_numpy(u_all[mine])
+    dist.all_reduce(out)
+    allcuts = [torch.zeros(world + 1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allcuts, torch.from_numpy(cuts))
+    if rank == 0:
+        q.put((out.numpy().tobytes() == u_all.tobytes(),
+               all(torch.equal(allcuts[0], c) for c in allcuts), cuts.tolist(), nwarps))
+    dist.destroy_process_group()
+
+
+def test_two_rank_shards_combine_bit_exactly():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    same, cuts_agree, cuts, nwarps = res
+    assert cuts_agree
+    assert cuts[0] == 0 and cuts[-1] == nwarps and 0 < cuts[1] < nwarps
+    assert same

@@ -1,0 +1,182 @@
+"""CPU: pin the oracle (oracle/stokes_oracle.c, the C restatement) to the reference.
+
+1. against the committed golden fixtures made by the reference itself
+   (tests/golden/make_golden.py over oracle/_ref) -- runs everywhere;
+2. against the reference compiled in place (oracle/_ref), where present;
+3. against the hand values of the reference's own unit tests."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import as_dict
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def inputs_for(S, name, g):
+    """Regenerate a fixture's inputs (or read the stored ones) and check the digest."""
+    specs = {"cfg0": ("cube", 10000, 12345, True), "small_noshrink": ("unit", 3000, 5, True),
+             "small_sto": ("unit", 2000, 62, False), "small_str": ("unit", 2000, 63, True),
+             "sphere_small": ("sphere", 8000, 12345, True), "mixture_disjoint": ("mixture", 6000, 12345, True),
+             "unit_n0_1": ("unit", 600, 3, True)}
+    if "in_position" in g.files:
+        d = {k: g["in_" + k] for k in ("position", "force_weight", "dipole_weight", "normal")
+             if "in_" + k in g.files}
+    else:
+        kind, n, seed, stre = specs[name]
+        ps = S.generate(kind, n, seed, stre)
+        d = as_dict(ps)
+    h = hashlib.sha256()
+    for k in ("position", "force_weight", "dipole_weight", "normal"):
+        if d.get(k) is not None:
+            h.update(np.ascontiguousarray(d[k]).tobytes())
+    assert h.hexdigest() == str(g["sha256"]), "generator output changed"
+    return d
+
+
+CASES = ["cfg0", "small_noshrink", "small_sto", "small_str", "sphere_small", "mixture_disjoint", "unit_n0_1"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_tree_matches_golden(S, O, name):
+    g = load(name)
+    d = inputs_for(S, name, g)
+    T = O.or_build_tree(d, int(g["n0"]), bool(g["shrink"]))
+    assert np.array_equal(T.to_original, g["perm"])
+    assert np.array_equal(np.stack([T.begin, T.end], 1), g["be"])
+    assert np.array_equal(T.geom.view(np.uint64), g["geom_bits"])
+    assert np.array_equal(T.children, g["children"])
+    assert np.array_equal(np.stack([T.n_children, T.is_leaf], 1), g["meta"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_treecode_matches_golden(S, O, name):
+    g = load(name)
+    d = inputs_for(S, name, g)
+    tg = g["targets"] if "targets" in g.files else None
+    u, st, pt = O.or_treecode(d, int(g["order"]), float(g["theta"]), int(g["n0"]), bool(g["shrink"]),
+                              bool(g["sto"]), bool(g["stre"]), targets=tg, per_target=True)
+    # the restatement follows the reference's arithmetic order: bit-exact
+    assert np.array_equal(u, g["u"])
+    assert np.array_equal(pt, g["per_target"].astype(np.uint64))
+    assert [st["farfield_evals"], st["direct_pairs"], st["clusters_visited"]] == list(g["stats"])
+
+
+def test_oracle_moments_match_golden(O):
+    g = load("moments_p3")
+    d = {k: g["in_" + k] for k in ("position", "force_weight", "dipole_weight", "normal")}
+    m = O.or_moments(d, 64, True, 3)
+    for k in ("stok", "str", "trace", "sym"):
+        assert np.array_equal(m[k], g[k]), k
+
+
+def test_oracle_farfield_matches_golden(O):
+    g = load("farfield_pairs")
+    for i, (p, dx) in enumerate(zip(g["p"], g["dx"])):
+        u = O.or_farfield_pair(dx, int(p), g[f"stok_{i}"], g[f"str_{i}"], g[f"trace_{i}"], g[f"sym_{i}"])
+        assert np.array_equal(u, g["u"][i])
+
+
+def test_oracle_coulomb_matches_golden(O):
+    g = load("coulomb")
+    for i, dx in enumerate(g["dx"]):
+        assert np.array_equal(O.or_coulomb(dx, 6), g[f"b{i}"])
+
+
+def test_oracle_direct_matches_golden(O):
+    g = load("direct")
+    d = {k: g["in_" + k] for k in ("position", "force_weight", "dipole_weight", "normal")}
+    tg = np.arange(len(d["position"]))
+    assert np.array_equal(O.or_direct_at(d, tg, True, True), g["u_both"])
+    assert np.array_equal(O.or_direct_at(d, tg, True, False), g["u_sto"])
+    assert np.array_equal(O.or_direct_at(d, tg, False, True), g["u_str"])
+    # contracted == naive tensor form at 1e-13 (test_kernels.cpp:158-175)
+    a, b = g["u_naive"], g["u_both"]
+    rel = np.linalg.norm(a - b, axis=1) / np.maximum(np.linalg.norm(a, axis=1), 1e-300)
+    assert rel.max() <= 1e-13
+
+
+# ---- hand values from the reference's unit tests
+def test_hand_values_coulomb(O):
+    # test_coulomb.cpp:11-25; graded-lex flat index: (0,0,0)=0, (0,0,1)=1, (0,1,0)=2, (1,0,0)=3
+    b = O.or_coulomb(np.array([1.0, 0, 0]), 3)
+    flat = lambda k1, k2, k3: {(0, 0, 0): 0, (0, 0, 1): 1, (0, 1, 0): 2, (1, 0, 0): 3}.get((k1, k2, k3))
+    assert b[flat(0, 0, 0)] == 1.0 and b[flat(1, 0, 0)] == 1.0 and b[flat(0, 1, 0)] == 0.0
+    assert b[9] == 1.0  # (2,0,0) is the last grade-2 entry: 4 + 5 = 9
+    b = O.or_coulomb(np.array([0.0, 2, 0]), 3)
+    assert b[0] == 0.5 and b[flat(0, 1, 0)] == 0.25
+    with pytest.raises(O.DomainError):
+        O.or_coulomb(np.zeros(3), 2)
+
+
+def test_hand_values_mac(O):
+    # test_cluster_tree.cpp:127-139
+    assert O.or_mac(1.0, 16.0, 0.5)
+    assert not O.or_mac(1.0, 2.25, 0.5)
+    assert not O.or_mac(1.0, 0.25, 0.99)
+    assert not O.or_mac(1.0, 0.0, 0.99)
+    assert O.or_mac(1.0, 4.0, 0.5)  # boundary r/R == theta is admissible
+
+
+def test_hand_values_direct(O):
+    # test_kernels.cpp:130-156 (contracted form gives the same exact values)
+    d = dict(position=np.array([[0, 0, 0], [1, 0, 0.0]]), force_weight=np.array([[1, 0, 0], [1, 0, 0.0]]))
+    assert np.array_equal(O.or_direct_at(d, [0, 1], True, False), [[2, 0, 0], [2, 0, 0]])
+    d = dict(position=np.array([[0, 0, 0], [1, 0, 0.0]]), force_weight=np.zeros((2, 3)),
+             dipole_weight=np.array([[1, 0, 0], [1, 0, 0.0]]), normal=np.array([[1, 0, 0], [1, 0, 0.0]]))
+    assert np.array_equal(O.or_direct_at(d, [0, 1], False, True), [[-1, 0, 0], [1, 0, 0]])
+    d = dict(position=np.array([[0, 0, 0], [1, 1, 1], [0, 0, 0.0]]), force_weight=np.ones((3, 3)))
+    with pytest.raises(O.DomainError):
+        O.or_direct_at(d, [0, 1, 2], True, False)
+
+
+def test_hand_values_relative_error(O):
+    # test_harness.cpp:26-60
+    ref = np.array([[1, 0, 0], [0, 1, 0.0]])
+    assert O.relative_error(ref, ref) == 0.0
+    assert O.relative_error(ref, np.zeros((2, 3))) == 1.0
+    assert abs(O.relative_error(ref, np.array([[1.1, 0, 0], [0, 1, 0]])) - 0.1 / np.sqrt(2)) < 1e-12
+    with pytest.raises(O.InvalidArgument):
+        O.relative_error(ref[:1], ref)
+    with pytest.raises(O.DomainError):
+        O.relative_error(np.zeros((1, 3)), np.ones((1, 3)))
+
+
+def test_eight_corners_tree(O):
+    # test_cluster_tree.cpp:63-83
+    pos = np.array([[x, y, z] for z in (0.0, 1.0) for y in (0.0, 1.0) for x in (0.0, 1.0)])
+    T = O.or_build_tree(dict(position=pos), 1, True)
+    assert T.ncl == 9 and T.n_children[0] == 8 and T.is_leaf.sum() == 8
+    assert np.all(T.radius[T.is_leaf == 1] == 0.0)
+
+
+def test_vanishing_theta_oracle(S, O):
+    # test_engine.cpp:12-24 on the restatement
+    d = as_dict(S.generate("unit", 1500, 9001, True))
+    u, st, _ = O.or_treecode(d, 5, 1e-9, 100)
+    direct = O.or_direct_at(d, np.arange(1500))
+    assert st["farfield_evals"] == 0
+    assert O.relative_error(direct, u) <= 1e-13
+
+
+# ---- live cross-check against the reference compiled in place (build container / GPU box)
+@pytest.mark.parametrize("kind,n,n0,shrink,p,theta", [
+    ("cube", 4000, 200, True, 6, 0.5), ("sphere", 5000, 300, False, 4, 0.7), ("mixture", 5000, 50, True, 8, 0.6),
+])
+def test_oracle_matches_reference_live(S, need_ref, kind, n, n0, shrink, p, theta):
+    O = need_ref
+    d = as_dict(S.generate(kind, n, 777, True))
+    ctx = O.RefContext(d, p, theta, n0, shrink)
+    u_ref, pt_ref, _ = ctx.eval(src_idx=np.arange(n), threads=os.cpu_count())
+    u, _, pt = O.or_treecode(d, p, theta, n0, shrink, per_target=True)
+    assert np.array_equal(u, u_ref) and np.array_equal(pt, pt_ref)
+    T = O.or_build_tree(d, n0, shrink)
+    R = ctx.tree()
+    assert np.array_equal(T.to_original, R.to_original)
+    assert np.array_equal(T.geom.view(np.uint64), R.geom.view(np.uint64))
