@@ -62,6 +62,8 @@ __device__ __forceinline__ void mi_decode(int e, int& k1, int& k2, int& k3) {
     k3 = s - k1 - k2;
 }
 
+// Thread t owns multi-indices t, t+T, ..., t+(EPT-1)T (T = blockDim.x, sized to E), so a
+// particle's 12 weights, read once as shared-memory broadcasts, feed 12*EPT FMAs.
 template <int EPT, bool STO, bool STR>
 __global__ void __launch_bounds__(kThreads)
     k_moments(int ncl_items, const int32_t* __restrict__ item_off, const int32_t* __restrict__ item_cl,
@@ -69,10 +71,12 @@ __global__ void __launch_bounds__(kThreads)
               const double* __restrict__ src, int p, int E, const int32_t* __restrict__ part_slot,
               double* __restrict__ M, double* __restrict__ part) {
     constexpr int NC = (STO ? 3 : 0) + (STR ? 9 : 0);
-    constexpr int C0 = STO ? 0 : 3;  // first combined column written
+    constexpr int NCP = (NC + 1) & ~1;  // padded to whole double2
+    constexpr int C0 = STO ? 0 : 3;     // first combined column written
     __shared__ double s_pow[kTileP][3 * kPow + 1];
-    __shared__ double s_w[kTileP][NC];
-    __shared__ int s_k[EPT * kThreads][3];
+    __shared__ __align__(16) double s_w[kTileP][NCP];
+    __shared__ int s_k[4 * kThreads][3];
+    const int T = blockDim.x;
 
     const int item = blockIdx.x;
     const int ci = find_item(item_off, ncl_items, item);  // index into the cluster list
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(kThreads)
     const int b = inf.x + chunk * kChunk;
     const int e_end = min(inf.y, b + kChunk);
 
-    for (int t = threadIdx.x; t < EPT * kThreads; t += kThreads) {
+    for (int t = threadIdx.x; t < EPT * T; t += T) {
         int k1 = 0, k2 = 0, k3 = 0;
         if (t < E) mi_decode(t, k1, k2, k3);
         s_k[t][0] = k1;
@@ -91,11 +95,11 @@ __global__ void __launch_bounds__(kThreads)
         s_k[t][2] = k3;
     }
 
-    double acc[EPT][NC];
+    double acc[EPT][NCP];
 #pragma unroll
     for (int j = 0; j < EPT; ++j)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[j][c] = 0.0;
+        for (int c = 0; c < NCP; ++c) acc[j][c] = 0.0;
 
     for (int t0 = b; t0 < e_end; t0 += kTileP) {
         const int nt = min(kTileP, e_end - t0);
@@ -118,16 +122,27 @@ __global__ void __launch_bounds__(kThreads)
                 for (int j = 0; j < 3; ++j)
                     for (int l = 0; l < 3; ++l)
                         s_w[threadIdx.x][(STO ? 3 : 0) + 3 * j + l] = r[6 + j] * r[9 + l];
+            if (NCP > NC) s_w[threadIdx.x][NCP - 1] = 0.0;
         }
         __syncthreads();
+        int kk[EPT][3];
 #pragma unroll
-        for (int j = 0; j < EPT; ++j) {
-            const int e = threadIdx.x + j * kThreads;
-            const int k1 = s_k[e][0], k2 = s_k[e][1], k3 = s_k[e][2];
-            for (int q = 0; q < nt; ++q) {
-                const double mono = s_pow[q][k1] * s_pow[q][kPow + k2] * s_pow[q][2 * kPow + k3];
+        for (int j = 0; j < EPT; ++j)
 #pragma unroll
-                for (int c = 0; c < NC; ++c) acc[j][c] = fma(mono, s_w[q][c], acc[j][c]);
+            for (int a = 0; a < 3; ++a) kk[j][a] = s_k[threadIdx.x + j * T][a];
+        for (int q = 0; q < nt; ++q) {
+            double w[NCP];
+#pragma unroll
+            for (int c = 0; c < NCP; c += 2) {
+                const double2 x = *reinterpret_cast<const double2*>(&s_w[q][c]);
+                w[c] = x.x;
+                w[c + 1] = x.y;
+            }
+#pragma unroll
+            for (int j = 0; j < EPT; ++j) {
+                const double mono = s_pow[q][kk[j][0]] * s_pow[q][kPow + kk[j][1]] * s_pow[q][2 * kPow + kk[j][2]];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) acc[j][c] = fma(mono, w[c], acc[j][c]);
             }
         }
     }
@@ -135,7 +150,7 @@ __global__ void __launch_bounds__(kThreads)
     double* out = slot < 0 ? M + (size_t)v * E * 12 : part + ((size_t)slot + chunk) * E * 12;
 #pragma unroll
     for (int j = 0; j < EPT; ++j) {
-        const int e = threadIdx.x + j * kThreads;
+        const int e = threadIdx.x + j * T;
         if (e < E) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) out[(size_t)e * 12 + C0 + c] = acc[j][c];
@@ -317,17 +332,17 @@ __global__ void k_import(int nblk, int E, int sto, int str, const double* __rest
 }
 
 template <int EPT>
-void launch_moments_ept(bool sto, bool str, dim3 g, cudaStream_t s, int ncl_items, const int32_t* off,
+void launch_moments_ept(bool sto, bool str, dim3 g, int threads, cudaStream_t s, int ncl_items, const int32_t* off,
                         const int32_t* cl, int nmulti, const int4* info, const double4* geom,
                         const double* src, int p, int E, const int32_t* slot, double* M, double* part) {
     if (sto && str)
-        k_moments<EPT, true, true><<<g, kThreads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
+        k_moments<EPT, true, true><<<g, threads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
                                                           slot, M, part);
     else if (sto)
-        k_moments<EPT, true, false><<<g, kThreads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
+        k_moments<EPT, true, false><<<g, threads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
                                                            slot, M, part);
     else
-        k_moments<EPT, false, true><<<g, kThreads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
+        k_moments<EPT, false, true><<<g, threads, 0, s>>>(ncl_items, off, cl, nmulti, info, geom, src, p, E,
                                                            slot, M, part);
     ST_LAUNCH("k_moments");
     count_launch();
@@ -363,16 +378,16 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
     M.alloc((size_t)ncl * E * 12, s);
     M.zero();
     DevArray<double> part((size_t)std::max(parts, 1) * E * 12, s);
-    const int ept = (E + kThreads - 1) / kThreads;
+    // entries per thread: 4 amortises the weight loads; block = E/EPT rounded up to a warp
+    const int ept = E >= 128 ? 4 : E >= 32 ? 2 : 1;
+    const int threads = std::max(32, ((E + ept - 1) / ept + 31) / 32 * 32);
     dim3 g(items);
     switch (ept) {
-        case 1: launch_moments_ept<1>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+        case 1: launch_moments_ept<1>(sto, str, g, threads, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
                                       tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
-        case 2: launch_moments_ept<2>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+        case 2: launch_moments_ept<2>(sto, str, g, threads, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
                                       tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
-        case 3: launch_moments_ept<3>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
-                                      tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
-        default: launch_moments_ept<4>(sto, str, g, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
+        default: launch_moments_ept<4>(sto, str, g, threads, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
                                        tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
     }
     if (parts) {
