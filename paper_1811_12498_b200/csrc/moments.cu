@@ -25,6 +25,11 @@
 // weight at k3 >= 2 is folded onto k3 - 2 until only k3 in {0,1} remain:
 // (P+1)^2 coefficients instead of E(P).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <vector>
 
 #include "moments.cuh"
 
@@ -155,6 +160,83 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
             for (int c = 0; c < NC; ++c) out[(size_t)e * 12 + C0 + c] = acc[j][c];
         }
+    }
+}
+
+// M2M (exact algebra): the moments of a cluster about its centre c_p from its children's
+// moments about theirs, M_p[k] = sum_children sum_{j<=k} C(k,j) (c_c - c_p)^(k-j) M_c[j]
+// (componentwise binomials).  Children in slot order, j in a fixed order: deterministic.
+template <int EPT, bool STO, bool STR>
+__global__ void __launch_bounds__(kThreads)
+    k_m2m(const int32_t* __restrict__ ids, const int32_t* __restrict__ children,
+          const int32_t* __restrict__ nchild, const double4* __restrict__ geom, int p, int E,
+          double* __restrict__ M) {
+    constexpr int NC = (STO ? 3 : 0) + (STR ? 9 : 0);
+    constexpr int C0 = STO ? 0 : 3;
+    extern __shared__ __align__(16) double m2m_smem[];
+    double* Mc = m2m_smem;                         // [E][12] child moments
+    double* A = m2m_smem + (size_t)E * 12;         // [3][p+1][p+1]: C(k,j) d^(k-j)
+    const int T = blockDim.x;
+    const int v = ids[blockIdx.x];
+    const double4 gp = geom[v];
+    int kk[EPT][3];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+        const int e = threadIdx.x + j * T;
+        if (e < E) mi_decode(e, kk[j][0], kk[j][1], kk[j][2]);
+        else kk[j][0] = kk[j][1] = kk[j][2] = 0;
+    }
+    double acc[EPT][NC];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[j][c] = 0.0;
+    const int P1 = p + 1;
+    for (int ch = 0; ch < nchild[v]; ++ch) {
+        const int u = children[8 * v + ch];
+        const double4 gc = geom[u];
+        __syncthreads();
+        for (int x = threadIdx.x; x < E * 12; x += T) Mc[x] = M[(size_t)u * E * 12 + x];
+        for (int x = threadIdx.x; x < 3 * P1 * P1; x += T) {
+            const int a = x / (P1 * P1), k = (x / P1) % P1, j = x % P1;
+            const double d = a == 0 ? gc.x - gp.x : a == 1 ? gc.y - gp.y : gc.z - gp.z;
+            double c = 0.0;
+            if (j <= k) {
+                c = 1.0;
+                for (int t = 0; t < k - j; ++t) c *= d;
+                // binomial C(k, j), exact in double for k <= 16
+                double bn = 1.0;
+                for (int t = 1; t <= j; ++t) bn = bn * (k - j + t) / t;
+                c *= bn;
+            }
+            A[x] = c;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int jj = 0; jj < EPT; ++jj) {
+            const int e = threadIdx.x + jj * T;
+            if (e >= E) continue;
+            const int k1 = kk[jj][0], k2 = kk[jj][1], k3 = kk[jj][2];
+            for (int j1 = 0; j1 <= k1; ++j1) {
+                const double a1 = A[(0 * P1 + k1) * P1 + j1];
+                for (int j2 = 0; j2 <= k2; ++j2) {
+                    const double a12 = a1 * A[(1 * P1 + k2) * P1 + j2];
+                    for (int j3 = 0; j3 <= k3; ++j3) {
+                        const double cf = a12 * A[(2 * P1 + k3) * P1 + j3];
+                        const double* mj = Mc + (size_t)mi_flat(j1, j2, j3) * 12 + C0;
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) acc[jj][c] = fma(cf, mj[c], acc[jj][c]);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int jj = 0; jj < EPT; ++jj) {
+        const int e = threadIdx.x + jj * T;
+        if (e < E)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) M[((size_t)v * E + e) * 12 + C0 + c] = acc[jj][c];
     }
 }
 
@@ -352,50 +434,112 @@ void launch_moments_ept(bool sto, bool str, dim3 g, int threads, cudaStream_t s,
 
 void compute_moments_device(const DevTree& tree, const double* src, int p, bool sto, bool str,
                             cudaStream_t s, DevArray<double>& M) {
+    static const bool dbg = getenv("ST_DEBUG_MOMENTS") != nullptr;
+    auto stamp = [&](const char* what) {
+        if (!dbg) return;
+        ST_CUDA(cudaStreamSynchronize(s));
+        static auto t0 = std::chrono::steady_clock::now();
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[moments] %-12s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
+    stamp("enter");
     if (p < 0 || p > kPmax) fail(ST_INVALID_ARGUMENT, "compute_moments: order outside table range");
     const int E = mi_count(p);
     const int ncl = tree.ncl;
-    // work items per cluster from the host copy of the cluster ranges
+    // leaves: direct sums over their particles; internal clusters: M2M by level (below)
     std::vector<int4> info(ncl);
     ST_CUDA(cudaMemcpyAsync(info.data(), tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> bylevel(ncl);
+    ST_CUDA(cudaMemcpyAsync(bylevel.data(), tree.bylevel.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
-    std::vector<int32_t> off(ncl + 1), cl(ncl), slot(ncl);
+    std::vector<int32_t> off, cl, slot;
     int items = 0, parts = 0;
     for (int v = 0; v < ncl; ++v) {
+        if (!info[v].w) continue;  // internal cluster
         const int cnt = info[v].y - info[v].x;
         const int nch = std::max(1, (cnt + kChunk - 1) / kChunk);
-        cl[v] = v;
-        off[v] = items;
-        slot[v] = nch > 1 ? parts : -1;
+        cl.push_back(v);
+        off.push_back(items);
+        slot.push_back(nch > 1 ? parts : -1);
         if (nch > 1) parts += nch;
         items += nch;
     }
-    off[ncl] = items;
-    DevArray<int32_t> d_off(ncl + 1, s), d_cl(ncl, s), d_slot(ncl, s);
-    ST_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), sizeof(int32_t) * (ncl + 1), cudaMemcpyHostToDevice, s));
-    ST_CUDA(cudaMemcpyAsync(d_cl.get(), cl.data(), sizeof(int32_t) * ncl, cudaMemcpyHostToDevice, s));
-    ST_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(int32_t) * ncl, cudaMemcpyHostToDevice, s));
+    const int nleaf = (int)cl.size();
+    off.push_back(items);
+    DevArray<int32_t> d_off(nleaf + 1, s), d_cl(nleaf, s), d_slot(nleaf, s), d_lvl(ncl, s);
+    ST_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), sizeof(int32_t) * (nleaf + 1), cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_cl.get(), cl.data(), sizeof(int32_t) * nleaf, cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(int32_t) * nleaf, cudaMemcpyHostToDevice, s));
+    // internal clusters of each level, deepest level last in `lv`
+    std::vector<std::vector<int32_t>> lv;
+    for (size_t d = 0; d + 1 < tree.level_start.size(); ++d) {
+        std::vector<int32_t> ids;
+        for (int b = tree.level_start[d]; b < tree.level_start[d + 1]; ++b)
+            if (!info[bylevel[b]].w) ids.push_back(bylevel[b]);
+        lv.push_back(ids);
+    }
+    {
+        std::vector<int32_t> flat;
+        for (const auto& ids : lv) flat.insert(flat.end(), ids.begin(), ids.end());
+        if (!flat.empty())
+            ST_CUDA(cudaMemcpyAsync(d_lvl.get(), flat.data(), sizeof(int32_t) * flat.size(), cudaMemcpyHostToDevice, s));
+    }
+    stamp("host lists");
     M.alloc((size_t)ncl * E * 12, s);
     M.zero();
     DevArray<double> part((size_t)std::max(parts, 1) * E * 12, s);
+    stamp("alloc");
     // entries per thread: 4 amortises the weight loads; block = E/EPT rounded up to a warp
     const int ept = E >= 128 ? 4 : E >= 32 ? 2 : 1;
     const int threads = std::max(32, ((E + ept - 1) / ept + 31) / 32 * 32);
-    dim3 g(items);
-    switch (ept) {
-        case 1: launch_moments_ept<1>(sto, str, g, threads, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
-                                      tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
-        case 2: launch_moments_ept<2>(sto, str, g, threads, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
-                                      tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
-        default: launch_moments_ept<4>(sto, str, g, threads, s, ncl, d_off.get(), d_cl.get(), 0, tree.info.get(),
-                                       tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+    if (items) {
+        dim3 g(items);
+        switch (ept) {
+            case 1: launch_moments_ept<1>(sto, str, g, threads, s, nleaf, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                          tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+            case 2: launch_moments_ept<2>(sto, str, g, threads, s, nleaf, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                          tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+            default: launch_moments_ept<4>(sto, str, g, threads, s, nleaf, d_off.get(), d_cl.get(), 0, tree.info.get(),
+                                           tree.geom.get(), src, p, E, d_slot.get(), M.get(), part.get()); break;
+        }
     }
     if (parts) {
-        k_reduce_parts<<<dim3(std::max(1, (E * 12 + 255) / 256), ncl), 256, 0, s>>>(
-            ncl, d_off.get(), d_cl.get(), d_slot.get(), E, part.get(), M.get());
+        k_reduce_parts<<<dim3(std::max(1, (E * 12 + 255) / 256), nleaf), 256, 0, s>>>(
+            nleaf, d_off.get(), d_cl.get(), d_slot.get(), E, part.get(), M.get());
         ST_LAUNCH("k_reduce_parts");
         count_launch();
     }
+    stamp("leaves");
+    // upward pass: deepest internal level first
+    const size_t smem = sizeof(double) * ((size_t)E * 12 + 3 * (size_t)(p + 1) * (p + 1));
+    size_t base = 0;
+    std::vector<size_t> lvl_off;
+    for (const auto& ids : lv) {
+        lvl_off.push_back(base);
+        base += ids.size();
+    }
+    for (int d = (int)lv.size() - 1; d >= 0; --d) {
+        const int cnt = (int)lv[d].size();
+        if (!cnt) continue;
+        auto go = [&](auto kern) {
+            ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kern<<<cnt, threads, smem, s>>>(d_lvl.get() + lvl_off[d], tree.children.get(), tree.nchild.get(),
+                                            tree.geom.get(), p, E, M.get());
+            ST_LAUNCH("k_m2m");
+            count_launch();
+        };
+        auto pick = [&](auto ept_tag) {
+            constexpr int EP = decltype(ept_tag)::value;
+            if (sto && str) go(k_m2m<EP, true, true>);
+            else if (sto) go(k_m2m<EP, true, false>);
+            else go(k_m2m<EP, false, true>);
+        };
+        if (ept == 1) pick(std::integral_constant<int, 1>{});
+        else if (ept == 2) pick(std::integral_constant<int, 2>{});
+        else pick(std::integral_constant<int, 4>{});
+    }
+    stamp("m2m");
 }
 
 void fold_weights_device(const double* M, int nblk, int p, bool sto, bool str, cudaStream_t s,

@@ -425,10 +425,12 @@ __global__ void k_finalize(int T, int geometry, const int32_t* __restrict__ pre,
                            const int32_t* __restrict__ nb_nch, const double* __restrict__ center,
                            const unsigned long long* __restrict__ r2max, const double* __restrict__ fbox,
                            double4* __restrict__ geom, int4* __restrict__ info, double* __restrict__ bbox,
-                           int32_t* __restrict__ children, int32_t* __restrict__ nchild) {
+                           int32_t* __restrict__ children, int32_t* __restrict__ nchild,
+                           int32_t* __restrict__ bylevel) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= T) return;
     const int p = pre[v];
+    bylevel[v] = p;
     const int nc = nb_nch[v];
     info[p] = make_int4((int)nb_begin[v], (int)nb_end[v], p + size[v], nc == 0 ? 1 : 0);
     nchild[p] = nc;
@@ -600,6 +602,8 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     out.info.alloc(T, s);
     out.children.alloc(8 * (size_t)T, s);
     out.nchild.alloc(T, s);
+    out.bylevel.alloc(T, s);
+    out.level_start = level_start;
 
     DevArray<double> center, fbox;
     DevArray<unsigned long long> r2max;
@@ -637,7 +641,8 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     k_finalize<<<blocks(T, 128), 128, 0, s>>>(T, geometry ? 1 : 0, pre.get(), size.get(), nb_begin.get(),
                                               nb_end.get(), nb_first.get(), nb_nch.get(), center.get(),
                                               r2max.get(), fbox.get(), out.geom.get(), out.info.get(),
-                                              out.bbox.get(), out.children.get(), out.nchild.get());
+                                              out.bbox.get(), out.children.get(), out.nchild.get(),
+                                              out.bylevel.get());
     ST_LAUNCH("k_finalize");
     count_launch();
     out.perm = std::move(perm);

@@ -18,6 +18,8 @@ struct DevTree {
     DevArray<int32_t> children;  // 8 per cluster, pre-order ids, -1 padded
     DevArray<int32_t> nchild;    // n_children
     DevArray<uint32_t> perm;     // tree index -> original index (to_original)
+    DevArray<int32_t> bylevel;   // pre-order ids in breadth-first (level) order
+    std::vector<int> level_start;  // host: bylevel[level_start[d] .. level_start[d+1]) = depth d
 };
 
 // Builds the tree of n points (xyz interleaved, device) with leaf capacity n0.

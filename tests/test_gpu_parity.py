@@ -64,7 +64,10 @@ def test_moments_match_reference(S, need_ref):
         for key, mine in (("stok", m.stok), ("str", m.str), ("trace", m.trace), ("sym", m.sym)):
             ref = r[key].reshape(mine.shape)
             scale = np.abs(ref).max(axis=(1, 2), keepdims=True) + 1e-300
-            assert np.max(np.abs(mine - ref) / scale) < 1e-13, (p, key)
+            # internal clusters come from the exact M2M shift of their children's moments,
+            # so sums are reassociated relative to the reference's particle-order sum:
+            # 1e-12 of the cluster's largest moment (observed <= 4e-13 at N = 20,000)
+            assert np.max(np.abs(mine - ref) / scale) < 1e-12, (p, key)
 
 
 def test_direct_matches_reference(S, need_ref):
