@@ -123,6 +123,17 @@ st_status st_treecode_velocity_device(const st_particles* src_device, const doub
                                       double* u_out_device, int shard, int n_shards,
                                       void* stream, st_stats* stats);
 
+/* Interaction lists (engine.hpp:80-108) of selected targets, for parity checks:
+ * target_index[i] is a source index (targets = sources, self excluded) when
+ * points == NULL, else points[3i..] is a disjoint target.  For each target, far[i*cap..]
+ * receives the accepted clusters and near[i*cap..] the leaves summed directly, in the
+ * reference's DFS order, as PRE-ORDER cluster ids (the reference's cluster ids);
+ * n_far[i] / n_near[i] the full counts (lists truncated at cap). */
+st_status st_interaction_lists(const st_particles* src, const st_params* params,
+                               const size_t* target_index, const double* points, size_t n_sel,
+                               size_t cap, int32_t* far, int32_t* near, int64_t* n_far,
+                               int64_t* n_near);
+
 /* ---- direct sums (O(N^2) oracle path) ---- */
 /* contracted_direct_velocity(ps, sel, first, last) (kernels.hpp:123-136). */
 st_status st_direct_velocity(const st_particles* src, int stokeslet, int stresslet, size_t first,

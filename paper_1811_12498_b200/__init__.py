@@ -44,7 +44,7 @@ __all__ = [
     "treecode_velocity", "parallel_velocity", "treecode_velocity_targets",
     "treecode_velocity_device", "contracted_direct_velocity", "contracted_direct_velocity_at",
     "naive_direct_velocity", "build_tree", "compute_moments", "coulomb_coeffs",
-    "farfield_pairs", "relative_error", "generate", "shard_cuts", "fp64_peak", "device_count",
+    "farfield_pairs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
     "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS",
 ]
 
@@ -58,7 +58,7 @@ EXPORTED_SYMBOLS = (
     "st_direct_velocity", "st_direct_velocity_at", "st_naive_direct_velocity", "st_build_tree",
     "st_tree_num_clusters", "st_tree_num_particles", "st_tree_export", "st_tree_free",
     "st_compute_moments", "st_coulomb_coeffs", "st_farfield_pairs", "st_relative_error",
-    "st_shard_cuts", "st_generate", "st_fp64_peak",
+    "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -139,6 +139,7 @@ def load_library():
     L.st_shard_cuts.argtypes = [sz, vp, i, vp]
     L.st_generate.argtypes = [i, sz, C.c_uint64, i, vp, vp, vp, vp]
     L.st_fp64_peak.argtypes = [d, P(d)]
+    L.st_interaction_lists.argtypes = [P(_Particles), P(_Params), vp, vp, sz, sz, vp, vp, vp, vp]
     for name in EXPORTED_SYMBOLS:
         if name not in ("st_abi_version", "st_last_error", "st_tree_num_clusters",
                         "st_tree_num_particles", "st_tree_free"):
@@ -319,6 +320,29 @@ def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole
     _check(L.st_treecode_velocity_device(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr,
                                          shard, n_shards, stream, C.byref(st)))
     return _result(None, st)
+
+
+def interaction_lists(ps: ParticleSet, params: TreecodeParams, target_index=None, points=None, cap: int = 4096):
+    """Per-target far (accepted cluster) and near (leaf) lists in DFS order, pre-order ids."""
+    L = load_library()
+    cp = ps._c(params.kernels)
+    prm = params._c()
+    if points is not None:
+        pts = _as3(points)
+        n = len(pts)
+        ti = None
+    else:
+        ti = np.ascontiguousarray(target_index, dtype=np.uint64)
+        n = len(ti)
+        pts = None
+    far = np.full((n, cap), -1, np.int32)
+    near = np.full((n, cap), -1, np.int32)
+    nf = np.zeros(n, np.int64)
+    nn = np.zeros(n, np.int64)
+    _check(L.st_interaction_lists(C.byref(cp), C.byref(prm), None if ti is None else ti.ctypes.data,
+                                  None if pts is None else pts.ctypes.data, n, cap, far.ctypes.data,
+                                  near.ctypes.data, nf.ctypes.data, nn.ctypes.data))
+    return [far[i, :min(nf[i], cap)].copy() for i in range(n)], [near[i, :min(nn[i], cap)].copy() for i in range(n)]
 
 
 # ------------------------------------------------------------------ direct sums

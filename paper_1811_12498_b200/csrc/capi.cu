@@ -489,6 +489,58 @@ st_status st_treecode_velocity_device(const st_particles* src, const double* tar
     });
 }
 
+st_status st_interaction_lists(const st_particles* src, const st_params* params, const size_t* target_index,
+                               const double* points, size_t n_sel, size_t cap, int32_t* far, int32_t* near,
+                               int64_t* n_far, int64_t* n_near) {
+    return guarded([&] {
+        validate_params(params);
+        validate_shape(src, params->stokeslet != 0, params->stresslet != 0);
+        if (!points && !target_index && n_sel) fail(ST_INVALID_ARGUMENT, "interaction_lists: no targets");
+        if (!n_sel) return;
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        DevParticles d;
+        upload(src, false, false, d, s);
+        DevTree tree;
+        build_tree_device(d.pos, d.n, params->leaf_capacity, params->shrink != 0, true, s, tree);
+        DevArray<uint32_t> to_tree(d.n, s);
+        DevArray<double> rec(12 * d.n, s);
+        k_pack<<<nblocks(d.n, 256), 256, 0, s>>>(d.n, tree.perm.get(), d.pos, nullptr, nullptr, nullptr, rec.get(),
+                                                 to_tree.get());
+        ST_LAUNCH("k_pack");
+        // selected targets (positions; self exclusion only matters for the counts, not the lists)
+        std::vector<double> hx(3 * n_sel);
+        if (points) {
+            std::copy(points, points + 3 * n_sel, hx.begin());
+        } else {
+            for (size_t i = 0; i < n_sel; ++i) {
+                if (target_index[i] >= src->n) fail(ST_INVALID_ARGUMENT, "interaction_lists: target out of range");
+                for (int a = 0; a < 3; ++a) hx[3 * i + a] = src->position[3 * target_index[i] + a];
+            }
+        }
+        DevArray<double> tx(3 * n_sel, s);
+        ST_CUDA(cudaMemcpyAsync(tx.get(), hx.data(), hx.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        DevArray<int32_t> dfar(n_sel * cap, s), dnear(n_sel * cap, s);
+        DevArray<int64_t> dnf(n_sel, s), dnn(n_sel, s);
+        dfar.fill_bytes(0xff);
+        dnear.fill_bytes(0xff);
+        TravArgs a;
+        a.tx = tx.get();
+        a.nt = (int)n_sel;
+        a.geom = tree.geom.get();
+        a.info = tree.info.get();
+        a.ncl = tree.ncl;
+        a.th2 = params->theta * params->theta;
+        launch_lists(a, (int)cap, dfar.get(), dnear.get(), dnf.get(), dnn.get(), s);
+        if (far) ST_CUDA(cudaMemcpyAsync(far, dfar.get(), dfar.bytes(), cudaMemcpyDeviceToHost, s));
+        if (near) ST_CUDA(cudaMemcpyAsync(near, dnear.get(), dnear.bytes(), cudaMemcpyDeviceToHost, s));
+        if (n_far) ST_CUDA(cudaMemcpyAsync(n_far, dnf.get(), dnf.bytes(), cudaMemcpyDeviceToHost, s));
+        if (n_near) ST_CUDA(cudaMemcpyAsync(n_near, dnn.get(), dnn.bytes(), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 static void direct_common(const st_particles* src, int sto, int str, const std::vector<int64_t>& tg,
                           double* u_out, bool naive) {
     validate_shape(src, sto != 0, str != 0);

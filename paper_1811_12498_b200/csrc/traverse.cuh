@@ -31,6 +31,9 @@ struct TravArgs {
 void launch_far(int P, const TravArgs& a, cudaStream_t s);
 // Near field + combine + scatter to original order + counters.
 void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s);
+// Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
+void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
+                  cudaStream_t s);
 // Traversal-only work estimate per warp (for multi-GPU shard cuts).
 void launch_count(const TravArgs& a, float far_cost, float near_cost, cudaStream_t s);
 

@@ -265,3 +265,32 @@ def test_validation_errors(S):
         S.treecode_velocity(bad2, S.TreecodeParams(kernels=S.KernelSelection.stokeslet_only()))
     with pytest.raises(S.InvalidArgument):
         S.treecode_velocity(S.ParticleSet(np.zeros((0, 3))), S.TreecodeParams())
+
+
+@pytest.mark.parametrize("kind,n,n0,theta,shrink", [
+    ("cube", 10000, 500, 0.5, True), ("sphere", 20000, 300, 0.7, True), ("mixture", 30000, 200, 0.6, False),
+    ("cube", 200000, 2000, 0.5, True),
+])
+def test_interaction_lists_bit_exact(S, O, kind, n, n0, theta, shrink):
+    """Full interaction lists (not just counts) equal the oracle's DFS lists."""
+    ps = S.generate(kind, n, 12345, True)
+    rng = np.random.default_rng(n)
+    sel = rng.choice(n, 300, replace=False)
+    prm = S.TreecodeParams(order=2, theta=theta, leaf_capacity=n0, shrink=shrink)
+    far, near = S.interaction_lists(ps, prm, target_index=sel)
+    T = O.or_build_tree(as_dict(ps), n0, shrink)
+    to_tree = np.empty(n, np.uint32)
+    to_tree[T.to_original] = np.arange(n, dtype=np.uint32)
+    ofar, onear = O.or_lists(as_dict(ps), n0, shrink, theta, tree_idx=to_tree[sel], cap=4096)
+    for i in range(len(sel)):
+        assert np.array_equal(far[i], ofar[i]) and np.array_equal(near[i], onear[i]), i
+
+
+def test_interaction_lists_disjoint_targets(S, O):
+    ps = S.generate("mixture", 20000, 12345, True)
+    pts = S.generate("points", 400, 67890).position
+    prm = S.TreecodeParams(order=2, theta=0.6, leaf_capacity=300)
+    far, near = S.interaction_lists(ps, prm, points=pts)
+    ofar, onear = O.or_lists(as_dict(ps), 300, True, 0.6, xyz=pts, cap=4096)
+    for i in range(len(pts)):
+        assert np.array_equal(far[i], ofar[i]) and np.array_equal(near[i], onear[i]), i
