@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "moments.cuh"
@@ -124,6 +125,17 @@ __global__ void k_targets(size_t nt, const uint32_t* __restrict__ tperm, const d
     tskip[t] = to_tree ? to_tree[o] : kNoSkip;
 }
 
+// batch order -> original order (multi-device gather on device 0)
+__global__ void k_unbatch(size_t nt, const uint32_t* __restrict__ torig, const double* __restrict__ ub,
+                          const uint64_t* __restrict__ pb, double* __restrict__ u, uint64_t* __restrict__ pt) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const size_t o = torig[t];
+    for (int a = 0; a < 3; ++a) u[3 * o + a] = ub[3 * t + a];
+    if (pt)
+        for (int a = 0; a < 3; ++a) pt[3 * o + a] = pb[3 * t + a];
+}
+
 // validate(ps, sel) (particles.hpp:41-70) on device: first failing index per check
 // {position finite, f finite, h finite, nu finite, nu unit (+-1e-12)}.
 __global__ void k_validate(size_t n, const double* __restrict__ pos, const double* __restrict__ f,
@@ -239,9 +251,14 @@ struct RunOut {
 
 void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
 
+struct ShardOut {
+    int w0 = 0, w1 = 0;         // warp (32-target batch) range evaluated
+    DevArray<uint32_t> torig;   // batch position -> original target index (if requested)
+};
+
 void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in, const st_params& prm,
                   double* d_out, uint64_t* d_per_target, int shard, int nshards, cudaStream_t s,
-                  RunOut& ro) {
+                  RunOut& ro, bool out_batch = false, ShardOut* so = nullptr) {
     const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
     const size_t n = src.n;
     const bool same = d_targets == nullptr;
@@ -304,6 +321,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     a.per_target = d_per_target;
     a.stats = d_stats.get();
     a.err = d_err.get();
+    a.out_batch = out_batch ? 1 : 0;
     const int P = prm.order + (str ? 2 : 1);
 
     if (nshards > 1) {
@@ -341,6 +359,11 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ro.t_total = secs(e0, e3);
     ro.t_far = secs(ef0, ef1);
     ro.t_near = secs(ef1, en1);
+    if (so) {
+        so->w0 = a.w0;
+        so->w1 = a.w1;
+        so->torig = std::move(torig);
+    }
 }
 
 void fill_stats(st_stats* st, const RunOut& ro) {
@@ -371,6 +394,101 @@ void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts) {
         cuts[sIdx] = std::max(cuts[sIdx - 1], i);
     }
     cuts[k] = n;
+}
+
+// Replicated-data multi-GPU in one process (PAPER.md:986-1030 with GPUs for MPI ranks):
+// one host thread per logical device uploads the inputs, rebuilds the (bit-identical)
+// tree and moments, evaluates its work-balanced shard of the Morton-ordered batches in
+// batch order and peer-copies that contiguous slice (NVLink P2P) into device 0, which
+// scatters the gathered batch-order velocities to original order.  Logical devices
+// beyond the physical count share GPUs round-robin (same results, no speedup).
+void multi_device(const st_particles* src, const double* targets, size_t n_targets, const st_params& prm,
+                  double* u_out, uint64_t* per_target, RunOut& ro_all, double& t_h2d, double& t_d2h) {
+    const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
+    const int D = prm.devices;
+    int ndev = 0;
+    ST_CUDA(cudaGetDeviceCount(&ndev));
+    const size_t nt = targets ? n_targets : src->n;
+    int dev0 = 0;
+    ST_CUDA(cudaGetDevice(&dev0));
+    OwnedStream os0;
+    cudaStream_t s0 = os0.s;
+    DevArray<double> gath(3 * nt, s0);
+    DevArray<uint64_t> gpt(per_target ? 3 * nt : 0, s0);
+    ST_CUDA(cudaStreamSynchronize(s0));  // allocations complete before other devices copy into them
+    std::vector<RunOut> ros(D);
+    std::vector<std::exception_ptr> errs(D);
+    ShardOut so0;
+    auto work = [&](int d) {
+        try {
+            const int dev = (dev0 + d) % ndev;
+            ST_CUDA(cudaSetDevice(dev));
+            ensure_device();
+            OwnedStream os;
+            cudaStream_t s = d == 0 ? s0 : os.s;
+            DevParticles dp;
+            upload(src, sto, str, dp, s);
+            DevArray<double> dt;
+            if (targets) {
+                dt.alloc(3 * nt, s);
+                ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
+            }
+            validate_values_device(dp.n, dp.pos, dp.f, dp.h, dp.nu, sto, str, s);
+            if (d == 0) {
+                run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, gath.get(), per_target ? gpt.get() : nullptr,
+                             0, D, s, ros[0], true, &so0);
+                ST_CUDA(cudaStreamSynchronize(s));
+                return;
+            }
+            DevArray<double> du(3 * nt, s);
+            DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s);
+            ShardOut so;
+            run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d, D,
+                         s, ros[d], true, &so);
+            const size_t t0 = (size_t)so.w0 * 32, t1 = std::min(nt, (size_t)so.w1 * 32);
+            if (t1 > t0) {
+                ST_CUDA(cudaMemcpyPeerAsync(gath.get() + 3 * t0, dev0, du.get() + 3 * t0, dev,
+                                            3 * (t1 - t0) * sizeof(double), s));
+                if (per_target)
+                    ST_CUDA(cudaMemcpyPeerAsync(gpt.get() + 3 * t0, dev0, dpt.get() + 3 * t0, dev,
+                                                3 * (t1 - t0) * sizeof(uint64_t), s));
+            }
+            ST_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            errs[d] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (int d = 1; d < D; ++d) th.emplace_back(work, d);
+    work(0);
+    for (auto& t : th) t.join();
+    ST_CUDA(cudaSetDevice(dev0));
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    Event d0, d1;
+    DevArray<double> du(3 * nt, s0);
+    DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s0);
+    k_unbatch<<<nblocks(nt, 256), 256, 0, s0>>>(nt, so0.torig.get(), gath.get(), gpt.get(), du.get(),
+                                                per_target ? dpt.get() : nullptr);
+    ST_LAUNCH("k_unbatch");
+    count_launch();
+    d0.record(s0);
+    ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s0));
+    if (per_target)
+        ST_CUDA(cudaMemcpyAsync(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), cudaMemcpyDeviceToHost, s0));
+    d1.record(s0);
+    ST_CUDA(cudaStreamSynchronize(s0));
+    t_d2h = secs(d0, d1);
+    t_h2d = 0.0;
+    for (const RunOut& r : ros) {
+        for (int k = 0; k < 3; ++k) ro_all.stats[k] += r.stats[k];
+        ro_all.t_build = std::max(ro_all.t_build, r.t_build);
+        ro_all.t_moments = std::max(ro_all.t_moments, r.t_moments);
+        ro_all.t_traverse = std::max(ro_all.t_traverse, r.t_traverse);
+        ro_all.t_total = std::max(ro_all.t_total, r.t_total);
+        ro_all.t_far = std::max(ro_all.t_far, r.t_far);
+        ro_all.t_near = std::max(ro_all.t_near, r.t_near);
+    }
 }
 
 }  // namespace
@@ -414,6 +532,18 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
         if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
         if (!u_out) fail(ST_INVALID_ARGUMENT, "u_out: null");
         ensure_device();
+        if (params->devices > 1) {
+            RunOut ro;
+            double th = 0, td = 0;
+            multi_device(src, targets, n_targets, *params, u_out, per_target, ro, th, td);
+            fill_stats(stats, ro);
+            if (stats) {
+                stats->time_h2d_s = th;
+                stats->time_d2h_s = td;
+                stats->gpu_launches = g_launches;
+            }
+            return;
+        }
         OwnedStream os;
         cudaStream_t s = os.s;
         Event h0, h1, d0, d1;

@@ -25,6 +25,7 @@ struct TravArgs {
     unsigned long long* stats = nullptr;  // {farfield_evals, direct_pairs, clusters_visited}
     int* err = nullptr;              // set to 1 on a coincident source/target pair
     float* warp_cost = nullptr;      // count pass: per-warp work estimate
+    int out_batch = 0;               // 1: write out / per_target in batch order (slot t), not torig[t]
 };
 
 // Far field for warps [w0, w1): P = p + 2 (stresslet) or p + 1.

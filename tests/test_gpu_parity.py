@@ -294,3 +294,19 @@ def test_interaction_lists_disjoint_targets(S, O):
     ofar, onear = O.or_lists(as_dict(ps), 300, True, 0.6, xyz=pts, cap=4096)
     for i in range(len(pts)):
         assert np.array_equal(far[i], ofar[i]) and np.array_equal(near[i], onear[i]), i
+
+
+@pytest.mark.parametrize("devices", [2, 3, 8])
+def test_multi_device_bit_identical(S, devices):
+    """params.devices > 1: shards on (logical) GPUs gathered over P2P; with one physical GPU
+    the logical devices share it.  Results must be bit-identical to one device, the
+    analogue of the reference's cross-worker identity (test_engine.cpp:48-70)."""
+    for kind, tg in (("cube", None), ("mixture", S.generate("points", 7000, 67890).position)):
+        ps = S.generate(kind, 30000, 5, True)
+        one = S.treecode_velocity_targets(ps, tg, S.TreecodeParams(order=6, theta=0.5, leaf_capacity=400),
+                                          per_target=True)
+        many = S.treecode_velocity_targets(ps, tg, S.TreecodeParams(order=6, theta=0.5, leaf_capacity=400,
+                                                                    devices=devices), per_target=True)
+        assert many.velocity.tobytes() == one.velocity.tobytes()
+        assert np.array_equal(many.per_target, one.per_target)
+        assert many.stats == one.stats
