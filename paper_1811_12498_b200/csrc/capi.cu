@@ -298,7 +298,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     count_launch();
 
     DevArray<unsigned long long> d_stats(3, s);
-    DevArray<int> d_err(1, s);
+    DevArray<int> d_err(1, s), d_work(2, s);
     d_stats.zero();
     d_err.zero();
 
@@ -322,6 +322,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     a.stats = d_stats.get();
     a.err = d_err.get();
     a.out_batch = out_batch ? 1 : 0;
+    a.work = d_work.get();
     const int P = prm.order + (str ? 2 : 1);
 
     if (nshards > 1) {

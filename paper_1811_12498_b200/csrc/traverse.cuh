@@ -26,6 +26,7 @@ struct TravArgs {
     int* err = nullptr;              // set to 1 on a coincident source/target pair
     float* warp_cost = nullptr;      // count pass: per-warp work estimate
     int out_batch = 0;               // 1: write out / per_target in batch order (slot t), not torig[t]
+    int* work = nullptr;             // persistent kernels: next batch counter (zeroed per launch)
 };
 
 // Far field for warps [w0, w1): P = p + 2 (stresslet) or p + 1.
