@@ -71,7 +71,8 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (wall time, line)
+        self.window = (0.0, float("inf"))
 
     def __enter__(self):
         try:
@@ -86,7 +87,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def wait_first(self, timeout=10.0):
+        """nvidia-smi's start-up disturbs the GPU briefly: let it settle before timing."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
+        time.sleep(0.3)
+
+    def mark(self, start, end):
+        self.window = (start, end)
 
     def __exit__(self, *a):
         if self.proc:
@@ -99,7 +110,9 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if not (self.window[0] <= ts <= self.window[1] + 0.15):
+                continue
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -244,6 +257,8 @@ def run_gpu(args, cfg):
         return r
 
     peak = S.fp64_peak(0.3)
+    clocks = ClockSampler(local).__enter__()
+    clocks.wait_first()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -252,22 +267,24 @@ def run_gpu(args, cfg):
     near_t = far_t = 0.0
     stats = None
     launches = 0
-    with ClockSampler(local) as clocks:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for k in range(args.steps):
-            flush.fill_(float(k))
-            ev[k][0].record(stream)
-            r = step()
-            ev[k][1].record(stream)
-            near_t += r.time_near_s
-            far_t += r.time_far_s
-            launches += r.gpu_launches
-            stats = r.stats
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = time.time()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ev[k][0].record(stream)
+        r = step()
+        ev[k][1].record(stream)
+        near_t += r.time_near_s
+        far_t += r.time_far_s
+        launches += r.gpu_launches
+        stats = r.stats
+    torch.cuda.synchronize()
+    clocks.mark(t_start, time.time())
+    if world > 1:
+        dist.barrier()
+    clocks.__exit__()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = float(sum(step_ms))
     t = torch.tensor([tot_ms, near_t, far_t], dtype=torch.float64, device=dev)
