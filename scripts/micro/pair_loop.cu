@@ -1,0 +1,77 @@
+// Microbenchmark: the near-field pair loop in isolation (smem-broadcast records, no
+// traversal), sweeping unroll depth and resident warps.  Same arithmetic as k_near.
+#include <cstdio>
+#include <cuda_runtime.h>
+__device__ __forceinline__ double rsqrt_dp(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x, y * y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+__device__ __forceinline__ double rsqrt_f32seed(double x) {
+    const float yf = rsqrtf(__double2float_rn(x));
+    const double y = (double)yf;
+    const double e = fma(-x, y * y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+template <bool F32>
+__device__ __forceinline__ void pair(const double* r, double x0, double x1, double x2, double& u0, double& u1,
+                                     double& u2, bool& bad) {
+    const double2 p01 = *reinterpret_cast<const double2*>(r);
+    const double2 p2f0 = *reinterpret_cast<const double2*>(r + 2);
+    const double d0 = x0 - p01.x, d1 = x1 - p01.y, d2 = x2 - p2f0.x;
+    const double rr = fma(d2, d2, fma(d1, d1, d0 * d0));
+    bad |= __double_as_longlong(rr) == 0;
+    const double rinv = F32 ? rsqrt_f32seed(rr) : rsqrt_dp(rr);
+    const double rinv2 = rinv * rinv;
+    const double2 f12 = *reinterpret_cast<const double2*>(r + 4);
+    const double2 h01 = *reinterpret_cast<const double2*>(r + 6);
+    const double2 h2n0 = *reinterpret_cast<const double2*>(r + 8);
+    const double2 n12 = *reinterpret_cast<const double2*>(r + 10);
+    const double f0 = p2f0.y, f1 = f12.x, f2 = f12.y;
+    const double df = fma(d2, f2, fma(d1, f1, d0 * f0));
+    const double dh = fma(d2, h2n0.x, fma(d1, h01.y, d0 * h01.x));
+    const double dn = fma(d2, n12.y, fma(d1, n12.x, d0 * h2n0.y));
+    const double sc = fma(dh * dn, rinv2, df) * rinv2;
+    u0 = fma(rinv, fma(d0, sc, f0), u0);
+    u1 = fma(rinv, fma(d1, sc, f1), u1);
+    u2 = fma(rinv, fma(d2, sc, f2), u2);
+}
+template <int U, bool F32>
+__global__ void kpair(double* out, int iters) {
+    __shared__ __align__(16) double rec[64 * 12];
+    for (int i = threadIdx.x; i < 64 * 12; i += blockDim.x) rec[i] = 0.1 + 0.01 * (i % 12) + 0.001 * (i / 12);
+    __syncthreads();
+    const double x0 = 1.0 + threadIdx.x * 1e-3, x1 = 2.0, x2 = 3.0;
+    double u[U][3] = {};
+    bool bad = false;
+    for (int it = 0; it < iters; ++it)
+        for (int q = 0; q < 64; q += U)
+#pragma unroll
+            for (int v = 0; v < U; ++v) pair<F32>(rec + 12 * (q + v), x0, x1, x2, u[v & 1][0], u[v & 1][1], u[v & 1][2], bad);
+    double s = 0;
+    for (int v = 0; v < 2 && v < U; ++v) s += u[v][0] + u[v][1] + u[v][2];
+    if (s == 1.2345 || bad) out[0] = s;
+}
+template <int U, bool F32 = false>
+void run(int threads, int blocks_per_sm, int iters) {
+    int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    double* o; cudaMalloc(&o, 8);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    const int grid = nsm * blocks_per_sm;
+    kpair<U, F32><<<grid, threads>>>(o, 2);
+    cudaEventRecord(e0);
+    kpair<U, F32><<<grid, threads>>>(o, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double pairs = (double)grid * threads * iters * 64;
+    printf("%s U=%d warps/SM=%2d: %.3e pairs/s = %.2f T DP-inst/s (30/pair)\n", F32 ? "f32seed" : "rsq64h ", U, threads / 32 * blocks_per_sm,
+           pairs / (ms * 1e-3), pairs * 30 / (ms * 1e-3) * 1e-12);
+}
+int main() {
+    for (int wps : {16, 24, 32}) {
+        run<4>(256, wps / 8, 400);
+        run<4, true>(256, wps / 8, 400);
+    }
+    return 0;
+}
