@@ -20,7 +20,6 @@ the velocities are combined with one NCCL collective.
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -63,71 +62,69 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled in-process through NVML (pynvml) every 200 ms
+    during the timed region (lighter than an nvidia-smi subprocess next to the step)."""
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
-        self.proc = None
-        self.lines = []  # (wall time, line)
+        self.lines = []  # (wall time, sm MHz, max MHz, reasons bitmask)
         self.window = (0.0, float("inf"))
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.N = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.lines.append((time.time(), sm, mx, rs))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
 
-    def wait_first(self, timeout=10.0):
-        """nvidia-smi's start-up disturbs the GPU briefly: let it settle before timing."""
+    def wait_first(self, timeout=5.0):
         t0 = time.time()
-        while self.proc and not self.lines and time.time() - t0 < timeout:
-            time.sleep(0.05)
-        time.sleep(0.3)
+        while self.t is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
 
     def mark(self, start, end):
         self.window = (start, end)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ts, ln in self.lines:
-            if not (self.window[0] <= ts <= self.window[1] + 0.15):
+        for ts, f, m, rs in self.lines:
+            if not (self.window[0] - 0.1 <= ts <= self.window[1] + 0.1):
                 continue
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
+            sm.append(float(f))
+            mx = float(m)
+            for nm, b in bits.items():
+                if rs & b:
                     reasons.add(nm)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0, "source": "nvml"}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml (pynvml), 200 ms"}
 
 
 def make_inputs(cfg):
@@ -267,6 +264,7 @@ def run_gpu(args, cfg):
     near_t = far_t = 0.0
     stats = None
     launches = 0
+    phases = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -280,6 +278,8 @@ def run_gpu(args, cfg):
         far_t += r.time_far_s
         launches += r.gpu_launches
         stats = r.stats
+        phases.append([round(1e3 * x, 2) for x in (r.time_build_s, r.time_moments_s, r.time_far_s, r.time_near_s,
+                                                   r.time_total_s)])
     torch.cuda.synchronize()
     clocks.mark(t_start, time.time())
     if world > 1:
@@ -338,7 +338,26 @@ def run_gpu(args, cfg):
         u_e2e = hout.numpy().copy()
         assert np.isfinite(u_e2e).all()
     e2e = {"value": e2e_val, "unit": "targets/s", "h2d_bytes_per_step": int(h2d_bytes) if rank == 0 else 0,
-           "d2h_bytes_per_step": int(d2h_bytes), "path": "st_treecode_velocity_device on pinned-host copies"}
+           "d2h_bytes_per_step": int(d2h_bytes),
+           "path": "st_treecode_velocity_device with per-step H2D of pinned particle arrays and D2H of the "
+                   "velocities (CUDA events, max over ranks)"}
+    if world == 1:
+        # the reference-facing host call itself (st_treecode_velocity, engine.hpp:194-196) on
+        # pinned host arrays: wall clock around the synchronous call, best of the timed steps
+        hp = hsrc.numpy()
+        pps = S.ParticleSet(hp[:n], hp[n:2 * n], hp[2 * n:3 * n], hp[3 * n:])
+        htgt = htg.numpy() if htg is not None else None
+        walls = []
+        for k in range(args.steps + 1):
+            t0 = time.perf_counter()
+            res = S.treecode_velocity_targets(pps, htgt, prm)
+            walls.append(time.perf_counter() - t0)
+        walls = walls[1:]
+        e2e["host_api"] = {"value": nt / float(np.median(walls)), "unit": "targets/s",
+                           "wall_ms_median": 1e3 * float(np.median(walls)),
+                           "call": "paper_1811_12498_b200.treecode_velocity -> st_treecode_velocity_ex",
+                           "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes)}
+        assert np.isfinite(res.velocity).all()
 
     # ---- roofline of the dominant kernel (near field), reference-algorithmic flops
     near_flops = F_NEAR * stats.direct_pairs
@@ -390,6 +409,7 @@ def run_gpu(args, cfg):
             "stats": {"farfield_evals": stats.farfield_evals, "direct_pairs": stats.direct_pairs,
                       "clusters_visited": stats.clusters_visited},
             "step_ms": step_ms,
+            "step_phases_ms": {"columns": ["build", "moments", "far", "near", "treecode_total"], "steps": phases},
         }
         print(json.dumps(line))
     if world > 1:

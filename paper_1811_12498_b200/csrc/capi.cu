@@ -45,29 +45,40 @@ st_status guarded(F&& f) {
 }
 
 // ------------------------------------------------------------ device context
-std::once_flag g_pool_once[64];
+
+// Per-device check done once (cudaGetDeviceProperties is slow and takes driver locks;
+// it must not sit inside every call's timed path).
+std::mutex g_dev_mu;
+int g_dev_state[64] = {0};  // 0 unknown, 1 ok, 2 wrong architecture
 
 void ensure_device() {
+    int dev = 0;
+    const cudaError_t e = cudaGetDevice(&dev);
     int ndev = 0;
-    const cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || ndev == 0)
+    if (e != cudaSuccess || cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
         fail(ST_CUDA_ERROR, std::string("no CUDA device available (") + cudaGetErrorString(e) +
                                 "); the treecode has no CPU fallback");
-    int dev = 0;
-    ST_CUDA(cudaGetDevice(&dev));
-    cudaDeviceProp prop;
-    ST_CUDA(cudaGetDeviceProperties(&prop, dev));
-    if (prop.major != 10)
-        fail(ST_CUDA_ERROR, "device " + std::to_string(dev) + " is sm_" + std::to_string(prop.major) +
-                                std::to_string(prop.minor) + "; this library is built for sm_100a");
-    if (dev < 64)
-        std::call_once(g_pool_once[dev], [dev] {
+    }
+    if (dev >= 64) return;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (g_dev_state[dev] == 0) {
+        int major = 0, minor = 0;
+        ST_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+        ST_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+        g_dev_state[dev] = major == 10 ? 1 : 2;
+        if (major == 10) {
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
                 uint64_t thr = UINT64_MAX;
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
             }
-        });
+        } else {
+            fail(ST_CUDA_ERROR, "device " + std::to_string(dev) + " is sm_" + std::to_string(major) +
+                                    std::to_string(minor) + "; this library is built for sm_100a");
+        }
+    }
+    if (g_dev_state[dev] == 2) fail(ST_CUDA_ERROR, "device is not sm_100; this library is built for sm_100a");
 }
 
 struct OwnedStream {
@@ -245,9 +256,24 @@ void upload(const st_particles* ps, bool need_f, bool need_hn, DevParticles& d, 
 
 // ------------------------------------------------------------ the treecode
 struct RunOut {
+    unsigned long long vflags[6] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull, ~0ull};  // first bad index per check
+    int domain_err = 0;
     uint64_t stats[3] = {0, 0, 0};
     double t_build = 0, t_moments = 0, t_traverse = 0, t_total = 0, t_far = 0, t_near = 0;
 };
+
+// validate(ps, sel) messages in the reference's order (particles.hpp:41-70), then the
+// coincident-pair domain error of the direct sums (kernels.hpp:52): validation first.
+void raise_flags(const RunOut& ro) {
+    const char* names[4] = {"position", "force_weight", "dipole_weight", "normal"};
+    for (int k = 0; k < 4; ++k)
+        if (ro.vflags[k] != ~0ull)
+            fail(ST_INVALID_ARGUMENT, std::string("particle array '") + names[k] + "' contains a non-finite value");
+    if (ro.vflags[4] != ~0ull) fail(ST_INVALID_ARGUMENT, "normal " + std::to_string(ro.vflags[4]) + " is not unit length");
+    if (ro.vflags[5] != ~0ull) fail(ST_INVALID_ARGUMENT, "targets: non-finite position");
+    if (ro.domain_err) fail(ST_DOMAIN_ERROR, "direct sum: coincident particles");
+}
+
 
 void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
 
@@ -256,9 +282,14 @@ struct ShardOut {
     DevArray<uint32_t> torig;   // batch position -> original target index (if requested)
 };
 
+// The particle arrays other than positions may still be in flight on another stream:
+// `weights_ready` (if set) is waited for after the tree build, which needs positions only.
+// Validation runs on the device after that wait and is read back with the results;
+// callers raise in the reference's order with raise_flags().
 void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in, const st_params& prm,
                   double* d_out, uint64_t* d_per_target, int shard, int nshards, cudaStream_t s,
-                  RunOut& ro, bool out_batch = false, ShardOut* so = nullptr) {
+                  RunOut& ro, bool out_batch = false, ShardOut* so = nullptr,
+                  cudaEvent_t weights_ready = nullptr) {
     const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
     const size_t n = src.n;
     const bool same = d_targets == nullptr;
@@ -270,6 +301,17 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     // K1: tree over the sources, tree-ordered source records
     DevTree tree;
     build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    if (weights_ready) ST_CUDA(cudaStreamWaitEvent(s, weights_ready, 0));
+    DevArray<unsigned long long> vflags(6, s);
+    vflags.fill_bytes(0xff);
+    k_validate<<<nblocks(n, 256), 256, 0, s>>>(n, src.pos, sto ? src.f : nullptr, str ? src.h : nullptr,
+                                                str ? src.nu : nullptr, str ? 1 : 0, vflags.get());
+    ST_LAUNCH("k_validate");
+    if (d_targets) {
+        k_validate<<<nblocks(nt_in, 256), 256, 0, s>>>(nt_in, d_targets, nullptr, nullptr, nullptr, 0, vflags.get() + 5);
+        ST_LAUNCH("k_validate");
+    }
+    count_launch(d_targets ? 2 : 1);
     DevArray<double> rec(12 * n, s);
     DevArray<uint32_t> to_tree(n, s);
     k_pack<<<nblocks(n, 256), 256, 0, s>>>(n, tree.perm.get(), src.pos, sto ? src.f : nullptr,
@@ -349,11 +391,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     en1.record(s);
     e3.record(s);
 
-    int herr = 0;
-    ST_CUDA(cudaMemcpyAsync(&herr, d_err.get(), sizeof herr, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaMemcpyAsync(ro.stats, d_stats.get(), sizeof ro.stats, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(ro.vflags, vflags.get(), sizeof ro.vflags, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
-    if (herr) fail(ST_DOMAIN_ERROR, "direct sum: coincident particles");
     ro.t_build = secs(e0, e1);
     ro.t_moments = secs(e1, e2);
     ro.t_traverse = secs(e2, e3);
@@ -434,11 +475,11 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
                 dt.alloc(3 * nt, s);
                 ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
             }
-            validate_values_device(dp.n, dp.pos, dp.f, dp.h, dp.nu, sto, str, s);
             if (d == 0) {
                 run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, gath.get(), per_target ? gpt.get() : nullptr,
                              0, D, s, ros[0], true, &so0);
                 ST_CUDA(cudaStreamSynchronize(s));
+                raise_flags(ros[0]);
                 return;
             }
             DevArray<double> du(3 * nt, s);
@@ -446,6 +487,7 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
             ShardOut so;
             run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d, D,
                          s, ros[d], true, &so);
+            raise_flags(ros[d]);
             const size_t t0 = (size_t)so.w0 * 32, t1 = std::min(nt, (size_t)so.w1 * 32);
             if (t1 > t0) {
                 ST_CUDA(cudaMemcpyPeerAsync(gath.get() + 3 * t0, dev0, du.get() + 3 * t0, dev,
@@ -545,44 +587,49 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
             }
             return;
         }
-        OwnedStream os;
-        cudaStream_t s = os.s;
-        Event h0, h1, d0, d1;
+        OwnedStream os, os2;
+        cudaStream_t s = os.s, s2 = os2.s;
+        Event h0, h1, wready, d0, d1;
         h0.record(s);
+        ST_CUDA(cudaStreamWaitEvent(s2, h0.e, 0));
+        // positions (and targets) first on the compute stream: the tree build needs only
+        // them; f, h, nu follow on a second stream and overlap the build
         DevParticles d;
-        upload(src, sto, str, d, s);
+        d.n = src->n;
+        auto up = [&](const double* hsrc, DevArray<double>& dst, cudaStream_t st) -> const double* {
+            if (!hsrc) return nullptr;
+            dst.alloc(3 * src->n, st);
+            ST_CUDA(cudaMemcpyAsync(dst.get(), hsrc, 3 * src->n * sizeof(double), cudaMemcpyHostToDevice, st));
+            return dst.get();
+        };
+        d.pos = up(src->position, d.own_pos, s);
         const size_t nt = targets ? n_targets : src->n;
         DevArray<double> dt;
         if (targets) {
             dt.alloc(3 * nt, s);
             ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
         }
-        h1.record(s);
-        validate_values_device(d.n, d.pos, d.f, d.h, d.nu, sto, str, s);
-        if (targets) {
-            DevArray<unsigned long long> bad(5, s);
-            bad.fill_bytes(0xff);
-            k_validate<<<nblocks(nt, 256), 256, 0, s>>>(nt, dt.get(), nullptr, nullptr, nullptr, 0, bad.get());
-            ST_LAUNCH("k_validate");
-            unsigned long long hb = 0;
-            ST_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
-            ST_CUDA(cudaStreamSynchronize(s));
-            if (hb != ~0ull) fail(ST_INVALID_ARGUMENT, "targets: non-finite position");
-        }
+        d.f = sto ? up(src->force_weight, d.own_f, s2) : nullptr;
+        d.h = str ? up(src->dipole_weight, d.own_h, s2) : nullptr;
+        d.nu = str ? up(src->normal, d.own_nu, s2) : nullptr;
+        wready.record(s2);
         DevArray<double> du(3 * nt, s);
         DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s);
         RunOut ro;
         run_treecode(d, targets ? dt.get() : nullptr, nt, *params, du.get(), per_target ? dpt.get() : nullptr, 0,
-                     1, s, ro);
+                     1, s, ro, false, nullptr, wready.e);
+        raise_flags(ro);
         d0.record(s);
         ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s));
         if (per_target)
             ST_CUDA(cudaMemcpyAsync(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         d1.record(s);
         ST_CUDA(cudaStreamSynchronize(s));
+        // stream-ordered frees of the s2 uploads must not race the compute stream
+        ST_CUDA(cudaStreamSynchronize(s2));
         fill_stats(stats, ro);
         if (stats) {
-            stats->time_h2d_s = secs(h0, h1);
+            stats->time_h2d_s = secs(h0, wready);
             stats->time_d2h_s = secs(d0, d1);
             stats->gpu_launches = g_launches;
         }
@@ -612,9 +659,9 @@ st_status st_treecode_velocity_device(const st_particles* src, const double* tar
         d.f = sto ? src->force_weight : nullptr;
         d.h = str ? src->dipole_weight : nullptr;
         d.nu = str ? src->normal : nullptr;
-        validate_values_device(d.n, d.pos, d.f, d.h, d.nu, sto, str, s);
         RunOut ro;
         run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro);
+        raise_flags(ro);
         fill_stats(stats, ro);
         if (stats) stats->gpu_launches = g_launches;
     });

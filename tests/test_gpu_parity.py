@@ -265,6 +265,14 @@ def test_validation_errors(S):
         S.treecode_velocity(bad2, S.TreecodeParams(kernels=S.KernelSelection.stokeslet_only()))
     with pytest.raises(S.InvalidArgument):
         S.treecode_velocity(S.ParticleSet(np.zeros((0, 3))), S.TreecodeParams())
+    # validation precedes the coincident-pair domain error, as in run_treecode (engine.hpp:133-135)
+    both = S.ParticleSet(ps.position.copy(), ps.force_weight, ps.dipole_weight, ps.normal.copy())
+    both.position[5] = both.position[6]
+    both.normal[9] *= 2.0
+    with pytest.raises(S.InvalidArgument, match="normal 9"):
+        S.treecode_velocity(both, S.TreecodeParams())
+    with pytest.raises(S.InvalidArgument, match="targets"):
+        S.treecode_velocity_targets(ps, np.array([[0.0, np.inf, 0.0]]), S.TreecodeParams())
 
 
 @pytest.mark.parametrize("kind,n,n0,theta,shrink", [
