@@ -123,6 +123,17 @@ st_status st_treecode_velocity_device(const st_particles* src_device, const doub
                                       double* u_out_device, int shard, int n_shards,
                                       void* stream, st_stats* stats);
 
+/* Order sweep (new): velocities at every order in orders[n_orders] (params->order
+ * ignored) from one tree, one moment pass at max(orders) -- order-p moments are the
+ * graded prefix of higher-order ones (multi_index.hpp:110-114) -- and one near-field
+ * pass (independent of p).  u_out[n_orders][3*n_t] in original order; each order's
+ * field is bit-identical to st_treecode_velocity_ex at that order.  far_seconds
+ * (optional, n_orders) receives each order's far-field kernel time.  stats are the
+ * traversal counters (identical for every order). */
+st_status st_treecode_velocity_sweep(const st_particles* src, const double* targets, size_t n_targets,
+                                     const st_params* params, const int* orders, int n_orders,
+                                     double* u_out, double* far_seconds, st_stats* stats);
+
 /* Interaction lists (engine.hpp:80-108) of selected targets, for parity checks:
  * target_index[i] is a source index (targets = sources, self excluded) when
  * points == NULL, else points[3i..] is a disjoint target.  For each target, far[i*cap..]

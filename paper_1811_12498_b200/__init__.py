@@ -42,7 +42,7 @@ __all__ = [
     "KernelSelection", "ParticleSet", "TreecodeParams", "TraversalStats", "VelocityResult",
     "ClusterTree", "ClusterMoments", "InvalidArgument", "DomainError", "StokesTreeError",
     "treecode_velocity", "parallel_velocity", "treecode_velocity_targets",
-    "treecode_velocity_device", "contracted_direct_velocity", "contracted_direct_velocity_at",
+    "treecode_velocity_device", "treecode_velocity_sweep", "contracted_direct_velocity", "contracted_direct_velocity_at",
     "naive_direct_velocity", "build_tree", "compute_moments", "coulomb_coeffs",
     "farfield_pairs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
     "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS",
@@ -58,7 +58,7 @@ EXPORTED_SYMBOLS = (
     "st_direct_velocity", "st_direct_velocity_at", "st_naive_direct_velocity", "st_build_tree",
     "st_tree_num_clusters", "st_tree_num_particles", "st_tree_export", "st_tree_free",
     "st_compute_moments", "st_coulomb_coeffs", "st_farfield_pairs", "st_relative_error",
-    "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists",
+    "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists", "st_treecode_velocity_sweep",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -139,6 +139,7 @@ def load_library():
     L.st_shard_cuts.argtypes = [sz, vp, i, vp]
     L.st_generate.argtypes = [i, sz, C.c_uint64, i, vp, vp, vp, vp]
     L.st_fp64_peak.argtypes = [d, P(d)]
+    L.st_treecode_velocity_sweep.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, vp, vp, P(_Stats)]
     L.st_interaction_lists.argtypes = [P(_Particles), P(_Params), vp, vp, sz, sz, vp, vp, vp, vp]
     for name in EXPORTED_SYMBOLS:
         if name not in ("st_abi_version", "st_last_error", "st_tree_num_clusters",
@@ -306,6 +307,26 @@ def treecode_velocity(ps: ParticleSet, params: TreecodeParams, per_target: bool 
 def parallel_velocity(ps: ParticleSet, params: TreecodeParams, per_target: bool = False) -> VelocityResult:
     """Replicated-data driver (engine.hpp:194-196); bit-identical to treecode_velocity."""
     return treecode_velocity_targets(ps, None, params, per_target)
+
+
+def treecode_velocity_sweep(ps: ParticleSet, params: TreecodeParams, orders, targets=None):
+    """Velocities at several orders from one tree / moment pass / near-field pass.
+
+    Returns (u[n_orders, n_t, 3], far_seconds[n_orders], VelocityResult with the shared
+    counters and phase times)."""
+    L = load_library()
+    cp = ps._c(params.kernels)
+    prm = params._c()
+    od = np.ascontiguousarray(orders, dtype=np.int32)
+    tg = _as3(targets) if targets is not None else None
+    nt = ps.size() if tg is None else len(tg)
+    u = np.zeros((len(od), nt, 3))
+    fs = np.zeros(len(od))
+    st = _Stats()
+    _check(L.st_treecode_velocity_sweep(C.byref(cp), None if tg is None else tg.ctypes.data,
+                                        0 if tg is None else len(tg), C.byref(prm), od.ctypes.data, len(od),
+                                        u.ctypes.data, fs.ctypes.data, C.byref(st)))
+    return u, fs, _result(None, st)
 
 
 def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],

@@ -136,6 +136,15 @@ __global__ void k_targets(size_t nt, const uint32_t* __restrict__ tperm, const d
     tskip[t] = to_tree ? to_tree[o] : kNoSkip;
 }
 
+// sweep: u_p = far_p + near for every target (same summation as the single-order path)
+__global__ void k_combine(size_t nt, const uint32_t* __restrict__ torig, const double* __restrict__ ufar,
+                          const double* __restrict__ unear, double* __restrict__ u) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const size_t o = torig[t];
+    for (int a = 0; a < 3; ++a) u[3 * o + a] = ufar[3 * t + a] + unear[3 * o + a];
+}
+
 // batch order -> original order (multi-device gather on device 0)
 __global__ void k_unbatch(size_t nt, const uint32_t* __restrict__ torig, const double* __restrict__ ub,
                           const uint64_t* __restrict__ pb, double* __restrict__ u, uint64_t* __restrict__ pt) {
@@ -438,6 +447,100 @@ void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts) {
     cuts[k] = n;
 }
 
+// Order sweep (SURVEY 8f "order-sweep reuse"): one tree, one moment pass at the largest
+// order (lower orders are graded prefixes), ONE near-field pass (it does not depend on
+// p), then per order only the fold + far field.  Each order's velocities are
+// bit-identical to a standalone call at that order.
+void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, const st_params& prm,
+               const int* orders, int n_orders, double* d_out /* n_orders x 3 nt, original order */,
+               double* far_s /* n_orders */, cudaStream_t s, RunOut& ro) {
+    const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
+    const size_t n = src.n;
+    const bool same = d_targets == nullptr;
+    const size_t nt = same ? n : nt_in;
+    int pmax = 0;
+    for (int i = 0; i < n_orders; ++i) pmax = std::max(pmax, orders[i]);
+    Event e0, e1, e2, e3;
+    e0.record(s);
+    DevTree tree;
+    build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    DevArray<unsigned long long> vflags(6, s);
+    vflags.fill_bytes(0xff);
+    k_validate<<<nblocks(n, 256), 256, 0, s>>>(n, src.pos, sto ? src.f : nullptr, str ? src.h : nullptr,
+                                                str ? src.nu : nullptr, str ? 1 : 0, vflags.get());
+    ST_LAUNCH("k_validate");
+    if (d_targets) {
+        k_validate<<<nblocks(nt, 256), 256, 0, s>>>(nt, d_targets, nullptr, nullptr, nullptr, 0, vflags.get() + 5);
+        ST_LAUNCH("k_validate");
+    }
+    DevArray<double> rec(12 * n, s);
+    DevArray<uint32_t> to_tree(n, s);
+    k_pack<<<nblocks(n, 256), 256, 0, s>>>(n, tree.perm.get(), src.pos, sto ? src.f : nullptr,
+                                           str ? src.h : nullptr, str ? src.nu : nullptr, rec.get(), to_tree.get());
+    ST_LAUNCH("k_pack");
+    count_launch(3);
+    e1.record(s);
+    DevArray<double> M;
+    compute_moments_device(tree, rec.get(), pmax, sto, str, s, M);
+    e2.record(s);
+    const double* tpos = same ? src.pos : d_targets;
+    DevTree ttree;
+    build_tree_device(tpos, nt, 32, false, false, s, ttree);
+    DevArray<double> tx(3 * nt, s), ufar(3 * nt, s), unear(3 * nt, s);
+    DevArray<uint32_t> torig(nt, s), tskip(nt, s);
+    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, ttree.perm.get(), tpos, same ? to_tree.get() : nullptr, tx.get(),
+                                               torig.get(), tskip.get());
+    ST_LAUNCH("k_targets");
+    count_launch();
+    DevArray<unsigned long long> d_stats(3, s);
+    DevArray<int> d_err(1, s), d_work(2, s);
+    d_stats.zero();
+    d_err.zero();
+    ufar.zero();
+    TravArgs a;
+    a.tx = tx.get();
+    a.tskip = tskip.get();
+    a.torig = torig.get();
+    a.nt = (int)nt;
+    a.w0 = 0;
+    a.w1 = (int)((nt + 31) / 32);
+    a.geom = tree.geom.get();
+    a.info = tree.info.get();
+    a.ncl = tree.ncl;
+    a.th2 = prm.theta * prm.theta;
+    a.src = rec.get();
+    a.ufar = ufar.get();  // zeros: the near pass stores near-field sums only
+    a.out = unear.get();
+    a.stats = d_stats.get();
+    a.err = d_err.get();
+    a.work = d_work.get();
+    launch_near(sto, str, a, s);
+    for (int i = 0; i < n_orders; ++i) {
+        Event f0, f1;
+        DevArray<double> W;
+        fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, s, W, pmax);
+        a.W = W.get();
+        a.out = nullptr;
+        f0.record(s);
+        launch_far(orders[i] + (str ? 2 : 1), a, s);
+        f1.record(s);
+        k_combine<<<nblocks(nt, 256), 256, 0, s>>>(nt, torig.get(), ufar.get(), unear.get(), d_out + 3 * nt * i);
+        ST_LAUNCH("k_combine");
+        count_launch();
+        ST_CUDA(cudaStreamSynchronize(s));
+        if (far_s) far_s[i] = secs(f0, f1);
+    }
+    e3.record(s);
+    ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(ro.stats, d_stats.get(), sizeof ro.stats, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(ro.vflags, vflags.get(), sizeof ro.vflags, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    ro.t_build = secs(e0, e1);
+    ro.t_moments = secs(e1, e2);
+    ro.t_traverse = secs(e2, e3);
+    ro.t_total = secs(e0, e3);
+}
+
 // Replicated-data multi-GPU in one process (PAPER.md:986-1030 with GPUs for MPI ranks):
 // one host thread per logical device uploads the inputs, rebuilds the (bit-identical)
 // tree and moments, evaluates its work-balanced shard of the Morton-ordered batches in
@@ -633,6 +736,41 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
             stats->time_d2h_s = secs(d0, d1);
             stats->gpu_launches = g_launches;
         }
+    });
+}
+
+st_status st_treecode_velocity_sweep(const st_particles* src, const double* targets, size_t n_targets,
+                                     const st_params* params, const int* orders, int n_orders, double* u_out,
+                                     double* far_seconds, st_stats* stats) {
+    return guarded([&] {
+        g_launches = 0;
+        validate_params(params);
+        if (!orders || n_orders < 1) fail(ST_INVALID_ARGUMENT, "sweep: no orders");
+        for (int i = 0; i < n_orders; ++i)
+            if (orders[i] < 0 || orders[i] > 16) fail(ST_INVALID_ARGUMENT, "params: order must be in [0, 16]");
+        const bool sto = params->stokeslet != 0, str = params->stresslet != 0;
+        validate_shape(src, sto, str);
+        if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
+        if (!u_out) fail(ST_INVALID_ARGUMENT, "u_out: null");
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        DevParticles d;
+        upload(src, sto, str, d, s);
+        const size_t nt = targets ? n_targets : src->n;
+        DevArray<double> dt;
+        if (targets) {
+            dt.alloc(3 * nt, s);
+            ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        DevArray<double> du(3 * nt * (size_t)n_orders, s);
+        RunOut ro;
+        run_sweep(d, targets ? dt.get() : nullptr, nt, *params, orders, n_orders, du.get(), far_seconds, s, ro);
+        raise_flags(ro);
+        ST_CUDA(cudaMemcpyAsync(u_out, du.get(), du.bytes(), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        fill_stats(stats, ro);
+        if (stats) stats->gpu_launches = g_launches;
     });
 }
 

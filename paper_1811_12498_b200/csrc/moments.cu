@@ -267,11 +267,11 @@ __device__ __forceinline__ double fact_ratio(int q, int k) {  // q!/k! for |q-k|
 // k3 >= 2 onto the harmonic basis, write W[blk][h][4].
 template <bool STO, bool STR>
 __global__ void __launch_bounds__(kThreads)
-    k_fold(int p, int P, const double* __restrict__ M, double* __restrict__ W) {
+    k_fold(int p, int P, int Estride, const double* __restrict__ M, double* __restrict__ W) {
     extern __shared__ double s_w[];  // [E(P)][4]
     const int EP = mi_count(P);
-    const int E = mi_count(p);
-    const double* Mb = M + (size_t)blockIdx.x * E * 12;
+    // moments of order p are the graded prefix of any higher-order block (multi_index.hpp:110-114)
+    const double* Mb = M + (size_t)blockIdx.x * Estride * 12;
     const double third = 1.0 / 3.0;
 
     for (int q = threadIdx.x; q < EP; q += blockDim.x) {
@@ -543,14 +543,14 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
 }
 
 void fold_weights_device(const double* M, int nblk, int p, bool sto, bool str, cudaStream_t s,
-                         DevArray<double>& W) {
+                         DevArray<double>& W, int pstride) {
     const int P = p + (str ? 2 : 1);
     const size_t smem = sizeof(double) * 4 * mi_count(P);
     W.alloc((size_t)nblk * harm_count(P) * 4, s);
     if (nblk == 0) return;
     auto go = [&](auto kern) {
         ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<nblk, kThreads, smem, s>>>(p, P, M, W.get());
+        kern<<<nblk, kThreads, smem, s>>>(p, P, mi_count(pstride < 0 ? p : pstride), M, W.get());
         ST_LAUNCH("k_fold");
         count_launch();
     };

@@ -16,8 +16,9 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
 // Far-field weights in the harmonic basis: W[ncl][(P+1)^2][4] with
 // u_i = sum_h b_h W[h][i] + dx_i * sum_h b_h W[h][3]  ("K4").
 // P = p + 2 with stresslets, p + 1 without.  `nblk` blocks of E(p) moments.
+// pstride: order the blocks of M were computed at (>= p; -1 = p).
 void fold_weights_device(const double* M, int nblk, int p, bool sto, bool str, cudaStream_t s,
-                         DevArray<double>& W);
+                         DevArray<double>& W, int pstride = -1);
 
 // Reference-layout export of M (stok[3E], str[9E], trace[E], sym[6E] per block;
 // moments.hpp:15-27, derive_stresslet_contractions :67-80).

@@ -318,3 +318,19 @@ def test_multi_device_bit_identical(S, devices):
         assert many.velocity.tobytes() == one.velocity.tobytes()
         assert np.array_equal(many.per_target, one.per_target)
         assert many.stats == one.stats
+
+
+def test_order_sweep_bit_identical_to_single_orders(S, need_ref):
+    """One tree / moment pass / near pass for several orders == separate calls, bit for bit."""
+    ps = S.generate("sphere", 20000, 12345, True)
+    orders = [2, 0, 5, 8]
+    prm = S.TreecodeParams(order=6, theta=0.7, leaf_capacity=400)
+    u, fs, res = S.treecode_velocity_sweep(ps, prm, orders)
+    assert np.all(fs > 0)
+    for i, p in enumerate(orders):
+        one = S.treecode_velocity(ps, S.TreecodeParams(order=p, theta=0.7, leaf_capacity=400))
+        assert u[i].tobytes() == one.velocity.tobytes(), p
+        assert res.stats == one.stats
+    ctx = need_ref.RefContext(as_dict(ps), 8, 0.7, 400, True)
+    u_ref, _, _ = ctx.eval(src_idx=np.arange(ps.size()), threads=8)
+    assert S.relative_error(u_ref, u[3]) <= REL_TOL
