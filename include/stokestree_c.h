@@ -206,6 +206,27 @@ enum {
 st_status st_generate(int kind, size_t n, uint64_t seed, int with_stresslets, double* pos,
                       double* f, double* h, double* nu);
 
+/* The paper's own test geometries (testcases.hpp:40-124), bit-identical to the reference:
+ * icosahedral sphere refined `levels` times (N = st_sphere_count(levels) = 20*4^levels;
+ * normals = positions; f, h uniform in [-1,1]) and Stokeslets uniform in a cube of side
+ * (n/density)^(1/3) (no stresslet arrays). */
+size_t st_sphere_count(int levels);
+st_status st_generate_sphere_icosa(int levels, uint64_t seed, double* pos, double* f, double* h,
+                                   double* nu);
+st_status st_generate_cube_density(size_t n, double density, uint64_t seed, double* pos, double* f);
+
+/* ---- particle text format (particle_io.hpp:30-126), host ---- */
+typedef struct st_loaded st_loaded;
+/* write_particles: validates like validate(ps, sel), header "x [f] [h nu]", "%.17g" fields. */
+st_status st_write_particles(const char* path, const st_particles* src, int stokeslet, int stresslet);
+/* read_particles: returns a handle, the particle count and the selection the header declares
+ * (errors: ST_RUNTIME_ERROR with the reference's message and line number). */
+st_status st_read_particles(const char* path, st_loaded** out, size_t* n, int* stokeslet,
+                            int* stresslet);
+/* copy the loaded arrays (3n doubles each; absent blocks leave their buffer untouched) */
+st_status st_loaded_copy(const st_loaded* loaded, double* pos, double* f, double* h, double* nu);
+void st_loaded_free(st_loaded* loaded);
+
 /* ---- measurement ---- */
 /* FP64 FMA throughput probe (a DFMA-only kernel over every SM): TFLOP/s with
  * FMA = 2 flop, run for roughly `seconds`. */

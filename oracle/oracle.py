@@ -124,6 +124,11 @@ def _load_ref():
         L.ref_coulomb.argtypes = [_dp, C.c_int, _dp]
         L.ref_farfield_pair.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _dp]
         L.ref_relative_error.argtypes = [_sz, _dp, _dp, C.POINTER(C.c_double)]
+        L.ref_sphere_particles.argtypes = [C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
+        L.ref_cube_particles.argtypes = [_sz, C.c_double, C.c_uint64, _dp, _dp]
+        L.ref_write_particles.argtypes = [C.c_char_p, _sz, _vp, _vp, _vp, _vp, C.c_int, C.c_int]
+        L.ref_read_particles.argtypes = [C.c_char_p, _sz, C.POINTER(_sz), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                         _dp, _dp, _dp, _dp]
         _ref = L
     return _ref
 
@@ -400,6 +405,35 @@ def ref_farfield_pair(dx, p, stok=None, strm=None, trace=None, sym=None):
                                          int(strm is not None), _opt(stok), _opt(strm), _opt(trace),
                                          _opt(sym), u), "ref_farfield_pair")
     return u
+
+
+def ref_sphere_particles(levels, seed):
+    n = 20 * 4 ** levels
+    a = [np.zeros((n, 3)) for _ in range(4)]
+    _check(_load_ref().ref_sphere_particles(levels, seed, *[x.reshape(-1) for x in a]), "ref_sphere_particles")
+    return dict(position=a[0], force_weight=a[1], dipole_weight=a[2], normal=a[3])
+
+
+def ref_cube_particles(n, density, seed):
+    a = [np.zeros((n, 3)) for _ in range(2)]
+    _check(_load_ref().ref_cube_particles(n, density, seed, a[0].reshape(-1), a[1].reshape(-1)), "ref_cube_particles")
+    return dict(position=a[0], force_weight=a[1])
+
+
+def ref_write_particles(path, ps, sto=True, stre=True):
+    n, p, _keep = _arrs(ps)
+    _check(_load_ref().ref_write_particles(os.fsencode(str(path)), n, p[0], p[1], p[2], p[3], int(sto), int(stre)),
+           "ref_write_particles")
+
+
+def ref_read_particles(path, cap):
+    a = [np.zeros((cap, 3)) for _ in range(4)]
+    n, sto, stre = C.c_size_t(), C.c_int(), C.c_int()
+    _check(_load_ref().ref_read_particles(os.fsencode(str(path)), cap, C.byref(n), C.byref(sto), C.byref(stre),
+                                          *[x.reshape(-1) for x in a]), "ref_read_particles")
+    k = n.value
+    return dict(position=a[0][:k], force_weight=a[1][:k] if sto.value else None,
+                dipole_weight=a[2][:k] if stre.value else None, normal=a[3][:k] if stre.value else None)
 
 
 # ---------------------------------------------------------------- seeded inputs (pure Python)

@@ -23,6 +23,8 @@
 #include "stokestree/kernels.hpp"
 #include "stokestree/moments.hpp"
 #include "stokestree/multi_index.hpp"
+#include "stokestree/particle_io.hpp"
+#include "stokestree/testcases.hpp"
 
 using namespace stokestree;
 
@@ -328,6 +330,53 @@ int ref_farfield_pair(const double* dx, int p, int sto, int str, const double* s
         u[0] = r[0];
         u[1] = r[1];
         u[2] = r[2];
+    });
+}
+
+// testcases.hpp:66-124 generators; arrays sized by the caller (sphere: 20*4^levels).
+int ref_sphere_particles(int levels, uint64_t seed, double* pos, double* f, double* h, double* nu) {
+    return guarded([&] {
+        const ParticleSet ps = sphere_particles({levels, seed});
+        for (std::size_t i = 0; i < ps.size(); ++i) {
+            put(pos, i, ps.position[i]);
+            put(f, i, ps.force_weight[i]);
+            put(h, i, ps.dipole_weight[i]);
+            put(nu, i, ps.normal[i]);
+        }
+    });
+}
+
+int ref_cube_particles(std::size_t n, double density, uint64_t seed, double* pos, double* f) {
+    return guarded([&] {
+        const ParticleSet ps = cube_particles({n, density, seed});
+        for (std::size_t i = 0; i < ps.size(); ++i) {
+            put(pos, i, ps.position[i]);
+            put(f, i, ps.force_weight[i]);
+        }
+    });
+}
+
+// particle_io.hpp: write with the reference writer; read back into caller arrays (n known).
+int ref_write_particles(const char* path, std::size_t n, const double* pos, const double* f, const double* h,
+                        const double* nu, int sto, int str) {
+    return guarded([&] { write_particles(path, make_ps(n, pos, f, h, nu), KernelSelection{sto != 0, str != 0}); });
+}
+
+int ref_read_particles(const char* path, std::size_t cap, std::size_t* n, int* sto, int* str, double* pos,
+                       double* f, double* h, double* nu) {
+    return guarded([&] {
+        const LoadedParticles L = read_particles(path);
+        *n = L.particles.size();
+        *sto = L.selection.stokeslet_enabled;
+        *str = L.selection.stresslet_enabled;
+        for (std::size_t i = 0; i < L.particles.size() && i < cap; ++i) {
+            put(pos, i, L.particles.position[i]);
+            if (*sto) put(f, i, L.particles.force_weight[i]);
+            if (*str) {
+                put(h, i, L.particles.dipole_weight[i]);
+                put(nu, i, L.particles.normal[i]);
+            }
+        }
     });
 }
 

@@ -45,7 +45,8 @@ __all__ = [
     "treecode_velocity_device", "treecode_velocity_sweep", "contracted_direct_velocity", "contracted_direct_velocity_at",
     "naive_direct_velocity", "build_tree", "compute_moments", "coulomb_coeffs",
     "farfield_pairs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
-    "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS",
+    "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS", "sphere_particles", "cube_particles",
+    "write_particles", "read_particles", "treecode_velocity_sweep",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -59,6 +60,8 @@ EXPORTED_SYMBOLS = (
     "st_tree_num_clusters", "st_tree_num_particles", "st_tree_export", "st_tree_free",
     "st_compute_moments", "st_coulomb_coeffs", "st_farfield_pairs", "st_relative_error",
     "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists", "st_treecode_velocity_sweep",
+    "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
+    "st_read_particles", "st_loaded_copy", "st_loaded_free",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -141,9 +144,18 @@ def load_library():
     L.st_fp64_peak.argtypes = [d, P(d)]
     L.st_treecode_velocity_sweep.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, vp, vp, P(_Stats)]
     L.st_interaction_lists.argtypes = [P(_Particles), P(_Params), vp, vp, sz, sz, vp, vp, vp, vp]
+    L.st_sphere_count.restype = sz
+    L.st_sphere_count.argtypes = [i]
+    L.st_generate_sphere_icosa.argtypes = [i, C.c_uint64, vp, vp, vp, vp]
+    L.st_generate_cube_density.argtypes = [sz, d, C.c_uint64, vp, vp]
+    L.st_write_particles.argtypes = [C.c_char_p, P(_Particles), i, i]
+    L.st_read_particles.argtypes = [C.c_char_p, P(vp), P(sz), P(i), P(i)]
+    L.st_loaded_copy.argtypes = [vp, vp, vp, vp, vp]
+    L.st_loaded_free.argtypes = [vp]
+    L.st_loaded_free.restype = None
     for name in EXPORTED_SYMBOLS:
         if name not in ("st_abi_version", "st_last_error", "st_tree_num_clusters",
-                        "st_tree_num_particles", "st_tree_free"):
+                        "st_tree_num_particles", "st_tree_free", "st_sphere_count", "st_loaded_free"):
             getattr(L, name).restype = i
     _lib = L
     return L
@@ -535,6 +547,55 @@ def generate(kind: str, n: int, seed: int, with_stresslets: bool = True) -> Part
     ptr = lambda x: None if x is None else x.ctypes.data
     _check(L.st_generate(k, n, seed, int(with_stresslets), pos.ctypes.data, f.ctypes.data, ptr(h), ptr(nu)))
     return ParticleSet(pos, f, h, nu)
+
+
+def sphere_particles(levels: int, seed: int) -> ParticleSet:
+    """The paper's icosahedral sphere geometry, N = 20 * 4^levels (testcases.hpp:66-106)."""
+    L = load_library()
+    if levels < 0:
+        raise InvalidArgument("sphere_particles: levels must be >= 0")
+    n = L.st_sphere_count(int(levels))
+    pos, f, h, nu = (np.zeros((n, 3)) for _ in range(4))
+    _check(L.st_generate_sphere_icosa(int(levels), seed, pos.ctypes.data, f.ctypes.data, h.ctypes.data,
+                                      nu.ctypes.data))
+    return ParticleSet(pos, f, h, nu)
+
+
+def cube_particles(n: int, density: float = 2500.0, seed: int = 0) -> ParticleSet:
+    """Stokeslets uniform in a cube of side (n/density)^(1/3) (testcases.hpp:108-124)."""
+    L = load_library()
+    if n < 1:
+        raise InvalidArgument("cube_particles: n must be >= 1")
+    if not density > 0:
+        raise InvalidArgument("cube_particles: density must be > 0")
+    pos, f = np.zeros((n, 3)), np.zeros((n, 3))
+    _check(L.st_generate_cube_density(int(n), float(density), seed, pos.ctypes.data, f.ctypes.data))
+    return ParticleSet(pos, f)
+
+
+def write_particles(path, ps: ParticleSet, sel: KernelSelection) -> None:
+    """write_particles (particle_io.hpp:34-58)."""
+    cp = ps._c(sel)
+    _check(load_library().st_write_particles(os.fsencode(str(path)), C.byref(cp), int(sel.stokeslet_enabled),
+                                             int(sel.stresslet_enabled)))
+
+
+def read_particles(path):
+    """read_particles (particle_io.hpp:60-126) -> (ParticleSet, KernelSelection)."""
+    L = load_library()
+    h = C.c_void_p()
+    n, sto, stre = C.c_size_t(), C.c_int(), C.c_int()
+    _check(L.st_read_particles(os.fsencode(str(path)), C.byref(h), C.byref(n), C.byref(sto), C.byref(stre)))
+    try:
+        pos = np.zeros((n.value, 3))
+        f = np.zeros((n.value, 3)) if sto.value else None
+        hh = np.zeros((n.value, 3)) if stre.value else None
+        nu = np.zeros((n.value, 3)) if stre.value else None
+        ptr = lambda x: None if x is None else x.ctypes.data
+        _check(L.st_loaded_copy(h.value, pos.ctypes.data, ptr(f), ptr(hh), ptr(nu)))
+    finally:
+        L.st_loaded_free(h.value)
+    return ParticleSet(pos, f, hh, nu), KernelSelection(bool(sto.value), bool(stre.value))
 
 
 def shard_cuts(weights, n_shards: int) -> np.ndarray:

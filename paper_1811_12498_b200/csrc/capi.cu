@@ -639,6 +639,13 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
 
 }  // namespace
 
+namespace st {
+st_status io_set_error(st_status s, const std::string& m) {
+    g_last_error = m;
+    return s;
+}
+}  // namespace st
+
 // ====================================================================== C ABI
 struct st_tree {
     OwnedStream own;  // declared first: destroyed after the arrays that free on it
