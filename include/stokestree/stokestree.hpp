@@ -573,3 +573,6 @@ inline double relative_error(std::span<const Vec3> u_ref, std::span<const Vec3> 
 }
 
 }  // namespace stokestree
+
+// The reference umbrella also brings in the harness layer (bench, particle_io, testcases).
+#include "stokestree/harness.hpp"
