@@ -334,3 +334,51 @@ def test_order_sweep_bit_identical_to_single_orders(S, need_ref):
     ctx = need_ref.RefContext(as_dict(ps), 8, 0.7, 400, True)
     u_ref, _, _ = ctx.eval(src_idx=np.arange(ps.size()), threads=8)
     assert S.relative_error(u_ref, u[3]) <= REL_TOL
+
+
+def test_depth_64_chain_tree_matches_reference(S, need_ref):
+    """Coincident points never separate: the reference recursion stops at depth 64
+    (cluster_tree.hpp:72, 96).  The level-synchronous build must reproduce that chain."""
+    ps = S.generate("unit", 500, 21, True)
+    pos = ps.position.copy()
+    pos[10] = pos[11] = pos[12] = pos[3]
+    dup = S.ParticleSet(pos, ps.force_weight, ps.dipole_weight, ps.normal)
+    T = S.build_tree(dup, 1, True)
+    ctx = need_ref.RefContext(as_dict(dup), 0, 0.5, 1, True)
+    tree_equal(T, ctx.tree())
+    deepest = T.ncl
+    assert deepest > 64 and T.is_leaf.sum() < 500  # a leaf holds the 4 coincident points
+    with pytest.raises(S.DomainError):
+        S.treecode_velocity(dup, S.TreecodeParams(order=2, leaf_capacity=1))
+
+
+def test_large_leaves_multi_chunk_moments(S, need_ref):
+    """Leaves above the 8,192-particle moment chunk use per-chunk partial sums."""
+    ps = S.generate("cube", 100000, 3, True)
+    T = S.build_tree(ps, 20000, True)
+    assert (T.end - T.begin)[T.is_leaf == 1].max() > 8192
+    m = S.compute_moments(T, 4, S.KernelSelection.both())
+    r = need_ref.RefContext(as_dict(ps), 4, 0.5, 20000, True).moments()
+    for key, mine in (("stok", m.stok), ("str", m.str)):
+        ref = r[key].reshape(mine.shape)
+        scale = np.abs(ref).max(axis=(1, 2), keepdims=True)
+        assert np.max(np.abs(mine - ref) / scale) < 1e-12
+    res = S.treecode_velocity(ps, S.TreecodeParams(order=4, theta=0.5, leaf_capacity=20000))
+    u_ref, _, _ = need_ref.ref_parallel_velocity(as_dict(ps), 4, 0.5, 20000, workers=8)
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_disjoint_target_on_a_source_is_a_domain_error(S):
+    ps = S.generate("cube", 2000, 8, True)
+    tg = np.vstack([S.generate("points", 10, 1).position, ps.position[17:18]])
+    with pytest.raises(S.DomainError):
+        S.treecode_velocity_targets(ps, tg, S.TreecodeParams(order=3, leaf_capacity=100))
+
+
+def test_n0_one_full_tree_parity(S, need_ref):
+    """Every leaf a single particle: all interactions are far field (test_cluster_tree)."""
+    ps = S.generate("mixture", 3000, 4, True)
+    res, u_ref, pt_ref, _ = run_pair(S, need_ref, ps, 3, 0.5, 1)
+    assert np.array_equal(res.per_target, pt_ref)
+    assert res.stats.direct_pairs == 0
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
