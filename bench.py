@@ -12,7 +12,8 @@ e2e   : the same metric through the public C ABI with pinned HOST buffers:
         H2D of the particle arrays, the treecode, D2H of the velocities.
 With torchrun (N > 1) every rank rebuilds the tree and moments (bit-identical)
 and evaluates its work-balanced shard of the Morton-ordered target batches;
-the velocities are combined with one NCCL collective.
+the batch-order slices are gathered with an NCCL all-gather over NVLink and scattered
+to original order.
 
 --impl reference runs the reference's own CPU treecode (the headers under
 /root/reference compiled in place, oracle/_ref/libstref.so) on the host cores.
@@ -125,6 +126,26 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0, "source": "nvml"}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm), "source": "nvml (pynvml), 200 ms"}
+
+
+def allgather_batch_slices(dist, ubatch, t0, t1, world):
+    """All-gather every rank's contiguous batch-order slice [t0, t1) of `ubatch` (n, 3) into
+    every rank's `ubatch` (one all-gather of the ranges, one all-gather of equal-length
+    padded slices; works on NCCL and gloo)."""
+    import torch
+    dev = ubatch.device
+    rng = torch.tensor([t0, t1], dtype=torch.int64, device=dev)
+    ranges = [torch.empty_like(rng) for _ in range(world)]
+    dist.all_gather(ranges, rng)
+    ranges = [tuple(int(v) for v in r.tolist()) for r in ranges]
+    maxlen = max(1, max(b - a for a, b in ranges))
+    send = torch.zeros((maxlen, 3), dtype=ubatch.dtype, device=dev)
+    send[: t1 - t0] = ubatch[t0:t1]
+    recv = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(recv, send)
+    for (a, b), piece in zip(ranges, recv):
+        ubatch[a:b] = piece[: b - a]
+    return ranges
 
 
 def make_inputs(cfg):
@@ -243,14 +264,22 @@ def run_gpu(args, cfg):
     stride = n * 3 * 8
     ptrs = (base, base + stride, base + 2 * stride, base + 3 * stride)
 
+    if world > 1:
+        dbatch = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
+        torig = torch.empty(nt, dtype=torch.int32, device=dev)
+
     def step():
-        dout.zero_()
-        r = S.treecode_velocity_device(*ptrs, n, prm, dout.data_ptr(),
-                                       targets_ptr=None if dtg is None else dtg.data_ptr(),
-                                       n_targets=nt if dtg is not None else 0, shard=rank, n_shards=world,
-                                       stream=sptr)
-        if world > 1:
-            dist.all_reduce(dout)  # disjoint shards: x + 0 + ... + 0 is exact
+        tp = None if dtg is None else dtg.data_ptr()
+        ntp = nt if dtg is not None else 0
+        if world == 1:
+            return S.treecode_velocity_device(*ptrs, n, prm, dout.data_ptr(), targets_ptr=tp, n_targets=ntp,
+                                              stream=sptr)
+        # every rank: same tree/moments, its work-balanced slice of the Morton-ordered batches in
+        # batch order; NCCL all-gather of the slices over NVLink; scatter to original order
+        t0, t1, r = S.treecode_shard_device(*ptrs, n, prm, dbatch.data_ptr(), torig.data_ptr(), targets_ptr=tp,
+                                            n_targets=ntp, shard=rank, n_shards=world, stream=sptr)
+        allgather_batch_slices(dist, dbatch, t0, t1, world)
+        S.unbatch_device(nt, torig.data_ptr(), dbatch.data_ptr(), dout.data_ptr(), stream=sptr)
         return r
 
     peak = S.fp64_peak(0.3)

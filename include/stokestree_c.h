@@ -145,6 +145,19 @@ st_status st_interaction_lists(const st_particles* src, const st_params* params,
                                size_t cap, int32_t* far, int32_t* near, int64_t* n_far,
                                int64_t* n_near);
 
+/* Shard evaluation for collective gathers (one rank per GPU): like
+ * st_treecode_velocity_device but the shard's velocities are written in BATCH order
+ * (Morton order of 32-target batches) into u_batch[3*t0 .. 3*t1), so every rank owns a
+ * contiguous slice [t0, t1) that an all-gather can move; batch_to_original (device,
+ * n_targets uint32, optional) receives the permutation, identical on every rank. */
+st_status st_treecode_shard_device(const st_particles* src_device, const double* targets_device,
+                                   size_t n_targets, const st_params* params, int shard, int n_shards,
+                                   double* u_batch_device, uint32_t* batch_to_original_device,
+                                   size_t* t0, size_t* t1, void* stream, st_stats* stats);
+/* u_out[3*batch_to_original[t] + a] = u_batch[3*t + a] for all t < n (device, stream). */
+st_status st_unbatch_device(size_t n, const uint32_t* batch_to_original_device,
+                            const double* u_batch_device, double* u_out_device, void* stream);
+
 /* ---- direct sums (O(N^2) oracle path) ---- */
 /* contracted_direct_velocity(ps, sel, first, last) (kernels.hpp:123-136). */
 st_status st_direct_velocity(const st_particles* src, int stokeslet, int stresslet, size_t first,

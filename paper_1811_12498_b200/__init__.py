@@ -61,7 +61,7 @@ EXPORTED_SYMBOLS = (
     "st_compute_moments", "st_coulomb_coeffs", "st_farfield_pairs", "st_relative_error",
     "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists", "st_treecode_velocity_sweep",
     "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
-    "st_read_particles", "st_loaded_copy", "st_loaded_free",
+    "st_read_particles", "st_loaded_copy", "st_loaded_free", "st_treecode_shard_device", "st_unbatch_device",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -144,6 +144,9 @@ def load_library():
     L.st_fp64_peak.argtypes = [d, P(d)]
     L.st_treecode_velocity_sweep.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, vp, vp, P(_Stats)]
     L.st_interaction_lists.argtypes = [P(_Particles), P(_Params), vp, vp, sz, sz, vp, vp, vp, vp]
+    L.st_treecode_shard_device.argtypes = [P(_Particles), vp, sz, P(_Params), i, i, vp, vp, P(sz), P(sz), vp,
+                                           P(_Stats)]
+    L.st_unbatch_device.argtypes = [sz, vp, vp, vp, vp]
     L.st_sphere_count.restype = sz
     L.st_sphere_count.argtypes = [i]
     L.st_generate_sphere_icosa.argtypes = [i, C.c_uint64, vp, vp, vp, vp]
@@ -339,6 +342,25 @@ def treecode_velocity_sweep(ps: ParticleSet, params: TreecodeParams, orders, tar
                                         0 if tg is None else len(tg), C.byref(prm), od.ctypes.data, len(od),
                                         u.ctypes.data, fs.ctypes.data, C.byref(st)))
     return u, fs, _result(None, st)
+
+
+def treecode_shard_device(position_ptr, force_ptr, dipole_ptr, normal_ptr, n, params, u_batch_ptr,
+                          batch_to_original_ptr=None, targets_ptr=None, n_targets=0, shard=0, n_shards=1,
+                          stream=0):
+    """Shard in batch order for all-gathers; returns (t0, t1, VelocityResult)."""
+    L = load_library()
+    cp = _Particles(n, position_ptr, force_ptr, dipole_ptr, normal_ptr)
+    prm = params._c()
+    st = _Stats()
+    t0, t1 = C.c_size_t(), C.c_size_t()
+    _check(L.st_treecode_shard_device(C.byref(cp), targets_ptr, n_targets, C.byref(prm), shard, n_shards,
+                                      u_batch_ptr, batch_to_original_ptr, C.byref(t0), C.byref(t1), stream,
+                                      C.byref(st)))
+    return t0.value, t1.value, _result(None, st)
+
+
+def unbatch_device(n, batch_to_original_ptr, u_batch_ptr, u_out_ptr, stream=0):
+    _check(load_library().st_unbatch_device(n, batch_to_original_ptr, u_batch_ptr, u_out_ptr, stream))
 
 
 def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],

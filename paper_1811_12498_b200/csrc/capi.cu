@@ -786,6 +786,54 @@ st_status st_treecode_velocity(const st_particles* src, const st_params* params,
     return st_treecode_velocity_ex(src, nullptr, 0, params, u_out, nullptr, stats);
 }
 
+st_status st_treecode_shard_device(const st_particles* src, const double* targets, size_t n_targets,
+                                   const st_params* params, int shard, int n_shards, double* u_batch,
+                                   uint32_t* batch_to_original, size_t* t0, size_t* t1, void* stream,
+                                   st_stats* stats) {
+    return guarded([&] {
+        g_launches = 0;
+        validate_params(params);
+        const bool sto = params->stokeslet != 0, str = params->stresslet != 0;
+        validate_shape(src, sto, str);
+        if (n_shards < 1 || shard < 0 || shard >= n_shards) fail(ST_INVALID_ARGUMENT, "shard out of range");
+        if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
+        if (!u_batch) fail(ST_INVALID_ARGUMENT, "u_batch: null");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevParticles d;
+        d.n = src->n;
+        d.pos = src->position;
+        d.f = sto ? src->force_weight : nullptr;
+        d.h = str ? src->dipole_weight : nullptr;
+        d.nu = str ? src->normal : nullptr;
+        const size_t nt = targets ? n_targets : src->n;
+        RunOut ro;
+        ShardOut so;
+        run_treecode(d, targets, nt, *params, u_batch, nullptr, shard, n_shards, s, ro, true, &so);
+        raise_flags(ro);
+        if (t0) *t0 = std::min(nt, (size_t)so.w0 * 32);
+        if (t1) *t1 = std::min(nt, (size_t)so.w1 * 32);
+        if (batch_to_original)
+            ST_CUDA(cudaMemcpyAsync(batch_to_original, so.torig.get(), nt * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                    s));
+        fill_stats(stats, ro);
+        if (stats) stats->gpu_launches = g_launches;
+    });
+}
+
+st_status st_unbatch_device(size_t n, const uint32_t* batch_to_original, const double* u_batch, double* u_out,
+                            void* stream) {
+    return guarded([&] {
+        if (!n) return;
+        if (!batch_to_original || !u_batch || !u_out) fail(ST_INVALID_ARGUMENT, "unbatch: null pointer");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        k_unbatch<<<nblocks(n, 256), 256, 0, s>>>(n, batch_to_original, u_batch, nullptr, u_out, nullptr);
+        ST_LAUNCH("k_unbatch");
+        count_launch();
+    });
+}
+
 st_status st_treecode_velocity_device(const st_particles* src, const double* targets, size_t n_targets,
                                       const st_params* params, double* u_out, int shard, int n_shards,
                                       void* stream, st_stats* stats) {

@@ -382,3 +382,34 @@ def test_n0_one_full_tree_parity(S, need_ref):
     assert np.array_equal(res.per_target, pt_ref)
     assert res.stats.direct_pairs == 0
     assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_shard_device_slices_assemble_bit_exactly(S):
+    """The one-rank-per-GPU entry: each shard's batch-order slice, assembled and unbatched,
+    equals the single-GPU field bit for bit (shards run one after another on this GPU)."""
+    import torch
+    ps = S.generate("cube", 40000, 9, True)
+    n = ps.size()
+    src = torch.from_numpy(np.concatenate([ps.position, ps.force_weight, ps.dipole_weight, ps.normal])).cuda()
+    b, stride = src.data_ptr(), n * 24
+    ptrs = (b, b + stride, b + 2 * stride, b + 3 * stride)
+    prm = S.TreecodeParams(order=6, theta=0.5, leaf_capacity=500)
+    stream = torch.cuda.current_stream().cuda_stream
+    full = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+    S.treecode_velocity_device(*ptrs, n, prm, full.data_ptr(), stream=stream)
+    world = 3
+    assembled = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+    torig = torch.empty(n, dtype=torch.int32, device="cuda")
+    covered = 0
+    for r in range(world):
+        part = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+        t0, t1, _ = S.treecode_shard_device(*ptrs, n, prm, part.data_ptr(), torig.data_ptr(), shard=r,
+                                            n_shards=world, stream=stream)
+        assert t0 == covered
+        covered = t1
+        assembled[t0:t1] = part[t0:t1]
+    assert covered == n
+    out = torch.zeros_like(full)
+    S.unbatch_device(n, torig.data_ptr(), assembled.data_ptr(), out.data_ptr(), stream=stream)
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)

@@ -1,8 +1,8 @@
 """CPU, world_size 2 over gloo: the N > 1 plumbing of bench.py / DESIGN.md "Multi-GPU".
 
 Every rank derives the same work-balanced cut of the Morton-ordered 32-target
-batches (no communication), owns a disjoint shard, and the velocity buffers are
-combined by one collective.  Because the shards are disjoint, x + 0 is exact and
+batches (no communication), owns a disjoint shard, and the batch-order slices
+are all-gathered (bench.allgather_batch_slices) and scattered to original order, so
 the combined result is bit-identical to the single-rank result.  The per-target
 velocities here come from the oracle (no GPU in this container); the CUDA path
 writes the same disjoint-shard layout."""
@@ -50,10 +50,15 @@ def _worker(rank, world, port, q):
         tg = order[32 * w:32 * (w + 1)]
         cost[w] = pt[tg, 1].sum() * 100 + pt[tg, 2].sum()
     cuts = S.shard_cuts(cost, world)
-    mine = order[32 * cuts[rank]:32 * cuts[rank + 1]]
+    # this rank's slice in batch order, gathered exactly as bench.py does it
+    from bench import allgather_batch_slices
+    t0, t1 = min(3000, 32 * int(cuts[rank])), min(3000, 32 * int(cuts[rank + 1]))
+    ubatch = torch.zeros((3000, 3), dtype=torch.float64)
+    ubatch[t0:t1] = torch.from_numpy(u_all[order[t0:t1]])
+    ranges = allgather_batch_slices(dist, ubatch, t0, t1, world)
+    assert ranges[0][0] == 0 and ranges[-1][1] == 3000
     out = torch.zeros((3000, 3), dtype=torch.float64)
-    out[torch.from_numpy(mine)] = torch.from_numpy(u_all[mine])
-    dist.all_reduce(out)
+    out[torch.from_numpy(order)] = ubatch  # the unbatch scatter (st_unbatch_device on a GPU)
     allcuts = [torch.zeros(world + 1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(allcuts, torch.from_numpy(cuts))
     if rank == 0:
