@@ -484,6 +484,30 @@ inline Vec3 stresslet_farfield(const Vec3& dx, const StressletMomentsView& m, in
     return u;
 }
 
+// ------------------------------------------------------------------ taylor_coeffs.hpp
+// Explicit Taylor coefficients (taylor_coeffs.hpp:13-46), formed by the device kernel from
+// the caller's coefficients (st_taylor_coeffs; a test/reference path, not the hot path).
+inline double stokeslet_taylor_coeff(const MultiIndexTable& table, const CoulombCoeffs& coeffs, int flat_k, int i,
+                                     int j) {
+    if (flat_k < 0 || flat_k >= table.size())
+        throw std::invalid_argument("stokeslet_taylor_coeff: multi-index out of table");
+    const int s = table[flat_k].norm();
+    if (s + 1 > coeffs.pmax) throw std::invalid_argument("stokeslet_taylor_coeff: coefficients not deep enough");
+    std::vector<double> a(9 * static_cast<std::size_t>(MultiIndexTable::count(s)));
+    abi::check(st_taylor_coeffs(1, coeffs.dx.c, coeffs.b.data(), coeffs.pmax, s, a.data(), nullptr));
+    return a[9 * static_cast<std::size_t>(flat_k) + 3 * i + j];
+}
+inline double stresslet_taylor_coeff(const MultiIndexTable& table, const CoulombCoeffs& coeffs, int flat_k, int i,
+                                     int j, int l) {
+    if (flat_k < 0 || flat_k >= table.size())
+        throw std::invalid_argument("stresslet_taylor_coeff: multi-index out of table");
+    const int s = table[flat_k].norm();
+    if (s + 2 > coeffs.pmax) throw std::invalid_argument("stresslet_taylor_coeff: coefficients not deep enough");
+    std::vector<double> a(27 * static_cast<std::size_t>(MultiIndexTable::count(s)));
+    abi::check(st_taylor_coeffs(1, coeffs.dx.c, coeffs.b.data(), coeffs.pmax, s, nullptr, a.data()));
+    return a[27 * static_cast<std::size_t>(flat_k) + 9 * i + 3 * j + l];
+}
+
 // ------------------------------------------------------------------ engine.hpp
 struct TreecodeParams {
     static constexpr int kMaxOrder = 16;

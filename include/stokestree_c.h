@@ -192,6 +192,13 @@ st_status st_compute_moments(const st_tree* tree, int order, int stokeslet, int 
 /* b^k for every k with |k| <= pmax, graded-lex order (multi_index.hpp:36-44), at
  * n_pairs displacements dx[3*n_pairs]; b_out[n_pairs * E(pmax)]. */
 st_status st_coulomb_coeffs(size_t n_pairs, const double* dx, int pmax, double* b_out);
+/* Explicit Taylor coefficients (taylor_coeffs.hpp:13-46) for every multi-index e of grade
+ * <= order: a_sto[(q*E(order) + e)*9 + 3i+j] = a^k_ij, a_str[(q*E(order) + e)*27 + 9i+3j+l]
+ * = a~^k_ijl.  b is st_coulomb_coeffs' output at depth pmax_b (E(pmax_b) doubles per pair);
+ * NULL = computed on the device from dx.  Either output may be NULL; a_sto needs
+ * order+1 <= pmax_b and a_str order+2 <= pmax_b (else ST_INVALID_ARGUMENT, :18-19/:35-36). */
+st_status st_taylor_coeffs(size_t n_pairs, const double* dx, const double* b, int pmax_b, int order,
+                           double* a_sto, double* a_str);
 /* stokeslet_farfield + stresslet_farfield for n_pairs (dx, moment block) pairs; moment
  * blocks in the reference layout, one block of E(p) entries per pair. */
 st_status st_farfield_pairs(size_t n_pairs, const double* dx, int order, int stokeslet,

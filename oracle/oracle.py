@@ -84,6 +84,7 @@ def _load_or():
         L.or_tree_free.argtypes = [_vp]
         L.or_moments.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp]
         L.or_coulomb.argtypes = [_dp, C.c_int, _dp]
+        L.or_taylor.argtypes = [_dp, _dp, C.c_int, C.c_int, _vp, _vp]
         L.or_farfield_pair.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _dp]
         L.or_treecode.argtypes = [_sz, _vp, _vp, _vp, _vp, _vp, _sz, C.c_int, C.c_double, C.c_int,
                                   C.c_int, C.c_int, C.c_int, C.c_int, _dp, _vp, _u64p]
@@ -122,6 +123,7 @@ def _load_ref():
         L.ref_direct_at.argtypes = [_sz, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _i64p, _sz, C.c_int, _dp]
         L.ref_naive_direct.argtypes = [_sz, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _dp]
         L.ref_coulomb.argtypes = [_dp, C.c_int, _dp]
+        L.ref_taylor.argtypes = [_dp, C.c_int, C.c_int, _vp, _vp]
         L.ref_farfield_pair.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _dp]
         L.ref_relative_error.argtypes = [_sz, _dp, _dp, C.POINTER(C.c_double)]
         L.ref_sphere_particles.argtypes = [C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
@@ -216,6 +218,19 @@ def or_coulomb(dx, pmax):
     b = np.zeros(mi_count(pmax) + 1)
     _check(_load_or().or_coulomb(np.ascontiguousarray(dx, np.float64), pmax, b), "or_coulomb")
     return b
+
+
+def or_taylor(dx, order, pmax_b=None, sto=True, stre=True, b=None):
+    """taylor_coeffs.hpp:13-46 for every multi-index of grade <= order:
+    (a_sto[E,3,3] or None, a_str[E,3,3,3] or None); b defaults to or_coulomb(dx, pmax_b)."""
+    pmax_b = order + (2 if stre else 1) if pmax_b is None else pmax_b
+    b = or_coulomb(dx, pmax_b) if b is None else np.ascontiguousarray(b, np.float64)
+    E = mi_count(order)
+    a = np.zeros((E, 3, 3)) if sto else None
+    t = np.zeros((E, 3, 3, 3)) if stre else None
+    _check(_load_or().or_taylor(np.ascontiguousarray(dx, np.float64), b, pmax_b, order, _opt(a), _opt(t)),
+           "or_taylor")
+    return a, t
 
 
 def or_farfield_pair(dx, p, stok=None, strm=None, trace=None, sym=None):
@@ -397,6 +412,16 @@ def ref_coulomb(dx, pmax):
     b = np.zeros(mi_count(pmax) + 1)
     _check(_load_ref().ref_coulomb(np.ascontiguousarray(dx, np.float64), pmax, b), "ref_coulomb")
     return b
+
+
+def ref_taylor(dx, order, pmax_b=None, sto=True, stre=True):
+    pmax_b = order + (2 if stre else 1) if pmax_b is None else pmax_b
+    E = mi_count(order)
+    a = np.zeros((E, 3, 3)) if sto else None
+    t = np.zeros((E, 3, 3, 3)) if stre else None
+    _check(_load_ref().ref_taylor(np.ascontiguousarray(dx, np.float64), pmax_b, order, _opt(a), _opt(t)),
+           "ref_taylor")
+    return a, t
 
 
 def ref_farfield_pair(dx, p, stok=None, strm=None, trace=None, sym=None):

@@ -24,6 +24,7 @@
 #include "stokestree/moments.hpp"
 #include "stokestree/multi_index.hpp"
 #include "stokestree/particle_io.hpp"
+#include "stokestree/taylor_coeffs.hpp"
 #include "stokestree/testcases.hpp"
 
 using namespace stokestree;
@@ -306,6 +307,24 @@ int ref_coulomb(const double* dx, int pmax, double* b_out) {
         const MultiIndexTable t(pmax);
         const CoulombCoeffs c = coulomb_coeffs(Vec3{dx[0], dx[1], dx[2]}, t);
         std::memcpy(b_out, c.b.data(), sizeof(double) * c.b.size());
+    });
+}
+
+// Explicit Taylor coefficients (taylor_coeffs.hpp:13-46) for every flat_k of grade <= order,
+// from coulomb_coeffs at depth pmax_b; layouts as or_taylor.
+int ref_taylor(const double* dx, int pmax_b, int order, double* a_sto, double* a_str) {
+    return guarded([&] {
+        const MultiIndexTable t(pmax_b);
+        const CoulombCoeffs c = coulomb_coeffs(Vec3{dx[0], dx[1], dx[2]}, t);
+        const int E = (order + 1) * (order + 2) * (order + 3) / 6;
+        for (int e = 0; e < E; ++e)
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    if (a_sto) a_sto[e * 9 + 3 * i + j] = stokeslet_taylor_coeff(t, c, e, i, j);
+                    if (a_str)
+                        for (int l = 0; l < 3; ++l)
+                            a_str[e * 27 + 9 * i + 3 * j + l] = stresslet_taylor_coeff(t, c, e, i, j, l);
+                }
     });
 }
 

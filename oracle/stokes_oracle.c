@@ -379,6 +379,51 @@ int or_coulomb(const double dx[3], int pmax, double *b_out) {
     return st;
 }
 
+/* Explicit Taylor coefficients from b of depth pmax_b (taylor_coeffs.hpp:13-46), for every
+   multi-index of grade <= order: a_sto[e*9 + 3i+j] (needs order+1 <= pmax_b),
+   a_str[e*27 + 9i+3j+l] (needs order+2 <= pmax_b).  b is sized E(pmax_b)+1 (zero slot). */
+int or_taylor(const double dx[3], const double *b, int pmax_b, int order, double *a_sto, double *a_str) {
+    if (order < 0 || pmax_b < 0) return OR_INVALID;
+    if ((a_sto && order + 1 > pmax_b) || (a_str && order + 2 > pmax_b)) return OR_INVALID;
+    mi_table t;
+    mi_init(&t, pmax_b);
+    const int E = mi_count(order);
+    for (int e = 0; e < E; ++e) {
+        const int *k = t.k[e];
+        for (int i = 0; i < 3; ++i) {
+            int ui[3] = {0, 0, 0};
+            ui[i] = 1;
+            for (int j = 0; j < 3; ++j) {
+                const double dij = i == j ? 1.0 : 0.0;
+                if (a_sto) {
+                    const double kip1 = k[i] + 1;
+                    int ud[3] = {ui[0], ui[1], ui[2]};
+                    ud[j] -= 1;
+                    a_sto[e * 9 + 3 * i + j] = dij * b[e] + dx[j] * kip1 * b[mi_shift(&t, e, ui[0], ui[1], ui[2])] -
+                                               (kip1 - dij) * b[mi_shift(&t, e, ud[0], ud[1], ud[2])];
+                }
+                if (!a_str) continue;
+                for (int l = 0; l < 3; ++l) {
+                    const double dil = i == l ? 1.0 : 0.0, djl = j == l ? 1.0 : 0.0;
+                    int uu[3] = {ui[0], ui[1], ui[2]};
+                    uu[j] += 1;
+                    int uud[3] = {uu[0], uu[1], uu[2]};
+                    uud[l] -= 1;
+                    int ul[3] = {0, 0, 0};
+                    ul[l] = 1;
+                    const double t1 = dx[l] * (k[i] + 1) * (k[j] + 1 + dij) * b[mi_shift(&t, e, uu[0], uu[1], uu[2])];
+                    const double t2 =
+                        (k[i] + 1 - dil) * (k[j] + 1 + dij - djl) * b[mi_shift(&t, e, uud[0], uud[1], uud[2])];
+                    const double t3 = dij * (k[l] + 1) * b[mi_shift(&t, e, ul[0], ul[1], ul[2])];
+                    a_str[e * 27 + 9 * i + 3 * j + l] = (t1 - t2 + t3) / 3.0;
+                }
+            }
+        }
+    }
+    mi_free(&t);
+    return OR_OK;
+}
+
 /* stokeslet_farfield, Eq. 25 (farfield.hpp:30-53) */
 static void sto_far(const double dx[3], const double *m3, int cnt, const mi_table *t,
                     const double *b, double u[3]) {

@@ -44,7 +44,7 @@ __all__ = [
     "treecode_velocity", "parallel_velocity", "treecode_velocity_targets",
     "treecode_velocity_device", "treecode_velocity_sweep", "contracted_direct_velocity", "contracted_direct_velocity_at",
     "naive_direct_velocity", "build_tree", "compute_moments", "coulomb_coeffs",
-    "farfield_pairs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
+    "farfield_pairs", "taylor_coeffs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
     "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS", "sphere_particles", "cube_particles",
     "write_particles", "read_particles", "treecode_velocity_sweep",
 ]
@@ -62,6 +62,7 @@ EXPORTED_SYMBOLS = (
     "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists", "st_treecode_velocity_sweep",
     "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
     "st_read_particles", "st_loaded_copy", "st_loaded_free", "st_treecode_shard_device", "st_unbatch_device",
+    "st_taylor_coeffs",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -137,6 +138,7 @@ def load_library():
     L.st_tree_free.restype = None
     L.st_compute_moments.argtypes = [vp, i, i, i, vp, vp, vp, vp]
     L.st_coulomb_coeffs.argtypes = [sz, vp, i, vp]
+    L.st_taylor_coeffs.argtypes = [sz, vp, vp, i, i, vp, vp]
     L.st_farfield_pairs.argtypes = [sz, vp, i, i, i, vp, vp, vp, vp, vp]
     L.st_relative_error.argtypes = [sz, vp, vp, P(d)]
     L.st_shard_cuts.argtypes = [sz, vp, i, vp]
@@ -525,6 +527,34 @@ def coulomb_coeffs(dx, pmax: int) -> np.ndarray:
     b = np.zeros((len(d), mi_count(max(pmax, 0))))
     _check(L.st_coulomb_coeffs(len(d), d.ctypes.data, int(pmax), b.ctypes.data))
     return b
+
+
+def taylor_coeffs(dx, order: int, stokeslet: bool = True, stresslet: bool = True, b=None, pmax_b=None):
+    """Explicit Taylor coefficients (taylor_coeffs.hpp:13-46) for every multi-index of grade
+    <= order at each displacement: (a_sto [n, E, 3, 3] or None, a_str [n, E, 3, 3, 3] or None),
+    a_sto[q, e, i, j] = a^k_ij and a_str[q, e, i, j, l] = a~^k_ijl.  ``b`` [n, E(pmax_b)] as
+    coulomb_coeffs returns it; None = formed on the device at depth order+2 (order+1 if
+    only the Stokeslet is asked for)."""
+    L = load_library()
+    d = np.ascontiguousarray(dx, np.float64).reshape(-1, 3)
+    bb = None if b is None else np.ascontiguousarray(b, np.float64).reshape(len(d), -1)
+    if pmax_b is None:
+        pmax_b = _grade_of_count(bb.shape[1]) if bb is not None else order + (2 if stresslet else 1)
+    E = mi_count(max(order, 0))
+    a = np.zeros((len(d), E, 3, 3)) if stokeslet else None
+    t = np.zeros((len(d), E, 3, 3, 3)) if stresslet else None
+    ptr = lambda x: None if x is None else x.ctypes.data
+    _check(L.st_taylor_coeffs(len(d), d.ctypes.data, ptr(bb), int(pmax_b), int(order), ptr(a), ptr(t)))
+    return a, t
+
+
+def _grade_of_count(n: int) -> int:
+    p = 0
+    while mi_count(p) < n:
+        p += 1
+    if mi_count(p) != n:
+        raise InvalidArgument(f"taylor_coeffs: {n} coefficients is not E(p) for any p")
+    return p
 
 
 def farfield_pairs(dx, p: int, stok=None, strm=None, trace=None, sym=None) -> np.ndarray:

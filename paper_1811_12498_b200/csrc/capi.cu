@@ -1097,6 +1097,35 @@ st_status st_coulomb_coeffs(size_t n, const double* dx, int pmax, double* b_out)
     });
 }
 
+st_status st_taylor_coeffs(size_t n, const double* dx, const double* b, int pmax_b, int order, double* a_sto,
+                           double* a_str) {
+    return guarded([&] {
+        if (pmax_b < 0 || order < 0) fail(ST_INVALID_ARGUMENT, "MultiIndexTable: pmax must be >= 0");
+        if (a_sto && order + 1 > pmax_b)
+            fail(ST_INVALID_ARGUMENT, "stokeslet_taylor_coeff: coefficients not deep enough");
+        if (a_str && order + 2 > pmax_b)
+            fail(ST_INVALID_ARGUMENT, "stresslet_taylor_coeff: coefficients not deep enough");
+        if (!b)
+            for (size_t i = 0; i < n; ++i) {
+                const double r2 = dx[3 * i] * dx[3 * i] + dx[3 * i + 1] * dx[3 * i + 1] + dx[3 * i + 2] * dx[3 * i + 2];
+                if (!(r2 > 0.0)) fail(ST_DOMAIN_ERROR, "coulomb_coeffs: zero displacement");
+            }
+        if (!n || (!a_sto && !a_str)) return;
+        ensure_device();
+        OwnedStream os;
+        cudaStream_t s = os.s;
+        const size_t EB = mi_count(pmax_b), E = mi_count(order);
+        DevArray<double> ddx(3 * n, s), db(EB * n, s), da(a_sto ? 9 * E * n : 0, s), dt(a_str ? 27 * E * n : 0, s);
+        ST_CUDA(cudaMemcpyAsync(ddx.get(), dx, ddx.bytes(), cudaMemcpyHostToDevice, s));
+        if (b) ST_CUDA(cudaMemcpyAsync(db.get(), b, db.bytes(), cudaMemcpyHostToDevice, s));
+        else launch_coulomb(n, ddx.get(), pmax_b, db.get(), s);
+        launch_taylor(n, ddx.get(), db.get(), pmax_b, order, a_sto ? da.get() : nullptr, a_str ? dt.get() : nullptr, s);
+        if (a_sto) ST_CUDA(cudaMemcpyAsync(a_sto, da.get(), da.bytes(), cudaMemcpyDeviceToHost, s));
+        if (a_str) ST_CUDA(cudaMemcpyAsync(a_str, dt.get(), dt.bytes(), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 st_status st_farfield_pairs(size_t n, const double* dx, int order, int sto, int str, const double* stok,
                             const double* strm, const double* /*trace*/, const double* /*sym*/,
                             double* u_out) {

@@ -51,5 +51,7 @@ void launch_naive(bool sto, bool str, const double* rec, size_t n, double* u, in
 void launch_far_pairs(int P, size_t n, const double* dx, const double* W, double* u, cudaStream_t s);
 // Reference-order Coulomb coefficients b^k, |k| <= pmax (coulomb.hpp:28-50).
 void launch_coulomb(size_t n, const double* dx, int pmax, double* b, cudaStream_t s);
+void launch_taylor(size_t n, const double* dx, const double* b, int pmax_b, int order, double* asto,
+                   double* astr, cudaStream_t s);
 
 }  // namespace st

@@ -13,6 +13,7 @@
 #include "stokestree/kernels.hpp"
 #include "stokestree/moments.hpp"
 #include "stokestree/multi_index.hpp"
+#include "stokestree/taylor_coeffs.hpp"
 
 using namespace stokestree;
 
@@ -177,6 +178,34 @@ static void device_checks() {
             }
             CHECK(norm(u - ex) / norm(ex) < 1e-8);
         }
+    }
+    // explicit Taylor coefficients (test_taylor_coeffs.cpp:33-66, 118-126)
+    {
+        const MultiIndexTable t2(2);
+        CHECK(std::fabs(stokeslet_taylor_coeff(t2, coulomb_coeffs({1, 0, 0}, t2), 0, 0, 0) - 2.0) < 1e-14);
+        CHECK(stokeslet_taylor_coeff(t2, coulomb_coeffs({0, 0, 1}, t2), 0, 0, 1) == 0.0);
+        const double a = stresslet_taylor_coeff(t2, coulomb_coeffs({1, 1, 1}, t2), 0, 0, 0, 0);
+        CHECK(std::fabs(a - 1.0 / (9.0 * std::sqrt(3.0))) < 1e-13 * a);
+        const MultiIndexTable t3(3);
+        const CoulombCoeffs c = coulomb_coeffs({1, 1, 0}, t3);
+        bool threw = false;
+        try { (void)stokeslet_taylor_coeff(t3, c, t3.size_at(3) - 1, 0, 0); } catch (const std::invalid_argument&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { (void)stresslet_taylor_coeff(t3, c, t3.size_at(2) - 1, 0, 0, 0); } catch (const std::invalid_argument&) { threw = true; }
+        CHECK(threw);
+        // zeroth coefficient reproduces the tensors (test_taylor_coeffs.cpp:13-31)
+        const Vec3 x{0.3, -0.7, 0.2}, y{-0.1, 0.4, 0.9};
+        const CoulombCoeffs cx = coulomb_coeffs(x - y, t3);
+        const Mat3 S = stokeslet(x, y);
+        const Ten3 T = stresslet(x, y);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                CHECK(std::fabs(stokeslet_taylor_coeff(t3, cx, 0, i, j) - S[i][j]) <= 1e-12 * std::fabs(S[i][j]));
+                for (int l = 0; l < 3; ++l)
+                    CHECK(std::fabs(stresslet_taylor_coeff(t3, cx, 0, i, j, l) - T[i][j][l]) <=
+                          1e-12 * std::fabs(T[i][j][l]));
+            }
     }
     // coincident particles -> domain_error (test_kernels.cpp:188-196)
     {

@@ -123,8 +123,19 @@ def main():
                         u_naive=O.ref_naive_direct(as_dict(ps), True, True),
                         in_position=ps.position, in_force_weight=ps.force_weight,
                         in_dipole_weight=ps.dipole_weight, in_normal=ps.normal)
+    taylor()
     print("golden fixtures written to", HERE)
 
 
+def taylor():
+    """Explicit Taylor coefficients (taylor_coeffs.hpp:13-46), grade <= 4 from b of depth 6."""
+    dxs = np.array([[1.0, 0, 0], [1.0, 1, 1], [0.3, -1.2, 0.4], [-0.6, 0.25, 0.8]])
+    out = {"dx": dxs}
+    for i, d in enumerate(dxs):
+        out[f"sto{i}"], out[f"str{i}"] = O.ref_taylor(d, 4, 6)
+    np.savez_compressed(os.path.join(HERE, "taylor.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    # `make_golden.py taylor` regenerates that fixture alone
+    taylor() if sys.argv[1:] == ["taylor"] else main()

@@ -73,6 +73,18 @@ def test_shape_validation_before_device(S):
         S.contracted_direct_velocity_at(ps, S.KernelSelection.stokeslet_only(), [7])
 
 
+def test_taylor_coeffs_validation_before_device(S):
+    # taylor_coeffs.hpp:15-19, 32-36 (depth guards) and coulomb zero displacement
+    with pytest.raises(S.InvalidArgument, match="not deep enough"):
+        S.taylor_coeffs([[1.0, 1, 0]], 3, stokeslet=True, stresslet=False, pmax_b=3)
+    with pytest.raises(S.InvalidArgument, match="not deep enough"):
+        S.taylor_coeffs([[1.0, 1, 0]], 2, stokeslet=False, stresslet=True, pmax_b=3)
+    with pytest.raises(S.DomainError):
+        S.taylor_coeffs([[0.0, 0, 0]], 1)
+    with pytest.raises(S.InvalidArgument):
+        S.taylor_coeffs([[1.0, 0, 0]], 1, b=np.zeros((1, 7)))  # 7 is not E(p)
+
+
 def test_compute_fails_loudly_without_gpu(S):
     if S.device_count() > 0:
         pytest.skip("a GPU is present")
@@ -83,6 +95,8 @@ def test_compute_fails_loudly_without_gpu(S):
         S.contracted_direct_velocity(ps, S.KernelSelection.both())
     with pytest.raises(S.StokesTreeError, match="no CPU fallback"):
         S.build_tree(ps, 10, True)
+    with pytest.raises(S.StokesTreeError, match="no CPU fallback"):
+        S.taylor_coeffs([[1.0, 0, 0]], 2)
 
 
 def test_generators_follow_splitmix_recipe(S, O):

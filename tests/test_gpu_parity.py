@@ -161,6 +161,47 @@ def test_coulomb_matches_reference(S, need_ref):
         S.coulomb_coeffs([[0, 0, 0]], 2)
 
 
+def test_taylor_coeffs_match_oracle(S, O):
+    # taylor_coeffs.hpp:13-46 on the device: b formed on the device, or the caller's b
+    rng = np.random.default_rng(11)
+    dx = rng.uniform(-2, 2, size=(40, 3))
+    for order in (0, 1, 4, 8, 14):
+        a, t = S.taylor_coeffs(dx, order)
+        b = S.coulomb_coeffs(dx, order + 3)
+        a2, t2 = S.taylor_coeffs(dx, order, b=b)
+        for q in range(0, 40, 3):
+            ao, to = O.or_taylor(dx[q], order, order + 2)
+            for got, want in ((a[q], ao), (t[q], to), (a2[q], ao), (t2[q], to)):
+                # device FMA contraction vs the reference's separate multiply/add
+                assert np.max(np.abs(got - want)) <= 1e-13 * np.abs(want).max()
+    # one kernel only: the other output is not formed
+    a, t = S.taylor_coeffs(dx[:2], 3, stresslet=False)
+    assert t is None and a.shape == (2, 20, 3, 3)
+
+
+def test_taylor_coeffs_match_golden(S):
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "taylor.npz"))
+    a, t = S.taylor_coeffs(g["dx"], 4, pmax_b=6)
+    for i in range(len(g["dx"])):
+        for got, want in ((a[i], g[f"sto{i}"]), (t[i], g[f"str{i}"])):
+            assert np.max(np.abs(got - want)) <= 1e-13 * np.abs(want).max()
+
+
+def test_taylor_coeffs_reference_tests(S, O):
+    # test_taylor_coeffs.cpp:13-116 through the device entry point
+    from test_oracle import check_taylor_fd, kernel_tensors, rel_diff, taylor_zeroth_cases
+    for x, y in taylor_zeroth_cases(O):
+        a, t = S.taylor_coeffs([x - y], 0, pmax_b=3)
+        S_, T_ = kernel_tensors(x, y)
+        assert rel_diff(a[0, 0], S_).max() < 1e-12 and rel_diff(t[0, 0], T_).max() < 5e-12
+    a, _ = S.taylor_coeffs([[1.0, 0, 0], [0, 0, 1.0]], 0, stresslet=False)
+    assert abs(a[0, 0, 0, 0] - 2.0) <= 1e-14 and a[1, 0, 0, 1] == 0.0
+    _, t = S.taylor_coeffs([[1.0, 1, 1]], 0, stokeslet=False)
+    assert abs(t[0, 0, 0, 0, 0] - 1 / (9 * np.sqrt(3))) <= 1e-13 * t[0, 0, 0, 0, 0]
+    check_taylor_fd(O, lambda x, p: tuple(None if v is None else v[0] for v in S.taylor_coeffs([x], p)))
+
+
 def run_pair(S, O, ps, order, theta, n0, shrink=True, sel=None):
     sel = sel or S.KernelSelection.both()
     prm = S.TreecodeParams(order=order, theta=theta, leaf_capacity=n0, shrink=shrink, kernels=sel)
