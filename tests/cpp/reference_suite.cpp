@@ -433,15 +433,21 @@ static void sphere_tree_structure() {
     check_partition(tree);
     for (const Vec3& p : tree.particles.position) CHECK(tree.root().bbox.contains(p));
 }
-// test_cluster_tree.cpp:116-125
+// test_cluster_tree.cpp:116-125.  The reference's own trees break this claim: with shrink
+// the centre moves to the tight box's midpoint and the radius about it can exceed the
+// unshrunk one -- 429 clusters over the three seeds (measured: this case compiled against
+// the reference headers).  Our trees are bit-exact with the reference's, so the case
+// pins that count: same cluster count, and exactly the reference's 429 violations.
 static void shrink_never_increases_radius() {
+    int violations = 0;
     for (uint64_t seed : {1u, 2u, 3u}) {
         const ParticleSet ps = random_particles(4000, seed, false);
         const ClusterTree plain = build_tree(ps, 50, false), shrunk = build_tree(ps, 50, true);
         CHECK(plain.clusters.size() == shrunk.clusters.size());
         for (std::size_t i = 0; i < std::min(plain.clusters.size(), shrunk.clusters.size()); ++i)
-            CHECK(shrunk.clusters[i].radius <= plain.clusters[i].radius);
+            violations += !(shrunk.clusters[i].radius <= plain.clusters[i].radius);
     }
+    CHECK(violations == 429);
 }
 // test_cluster_tree.cpp:165-179
 static void single_particle_moments() {
@@ -456,7 +462,11 @@ static void single_particle_moments() {
         for (int j = 0; j < 3; ++j) CHECK(sv.m[3 * e + j] == 0.0);
     CHECK(sv.m[0] == 1.0 && sv.m[1] == 2.0 && sv.m[2] == 3.0);
 }
-// test_cluster_tree.cpp:181-218
+// test_cluster_tree.cpp:181-218.  The reference's own stresslet moments differ from this
+// pow() loop by up to 2.054e-13 (measured against the reference headers), above the
+// case's 1e-14; the Stokeslet ones stay at 5e-16.  The device sums particles in a
+// parallel order with FMA, so a cancelling entry can also leave 1e-14 here; the bound is
+// 1e-12 (north_star's velocity bar) for every moment and contraction.
 static void moments_definitional_loop() {
     const ParticleSet ps = random_particles(100, 77, true);
     const ClusterTree tree = build_tree(ps, 200, false);
@@ -480,13 +490,13 @@ static void moments_definitional_loop() {
             }
         }
         for (int j = 0; j < 3; ++j) {
-            CHECK(rel_diff(sv.m[3 * e + j], ms[j]) < 1e-14);
-            for (int l = 0; l < 3; ++l) CHECK(rel_diff(tv.mt[9 * e + 3 * j + l], mt[j][l]) < 1e-14);
+            CHECK(rel_diff(sv.m[3 * e + j], ms[j]) < 1e-12);
+            for (int l = 0; l < 3; ++l) CHECK(rel_diff(tv.mt[9 * e + 3 * j + l], mt[j][l]) < 1e-12);
         }
-        CHECK(rel_diff(tv.trace[e], mt[0][0] + mt[1][1] + mt[2][2]) < 1e-14);
+        CHECK(rel_diff(tv.trace[e], mt[0][0] + mt[1][1] + mt[2][2]) < 1e-12);
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j)
-                CHECK(rel_diff(tv.sym[6 * e + MultiIndexTable::sym_index(i, j)], mt[i][j] + mt[j][i]) < 1e-14);
+                CHECK(rel_diff(tv.sym[6 * e + MultiIndexTable::sym_index(i, j)], mt[i][j] + mt[j][i]) < 1e-12);
     }
 }
 // test_farfield.cpp:21-47
@@ -572,7 +582,14 @@ static void farfield_zero_dipoles() {
         CHECK(stresslet_farfield(dx, m.stresslet_view(0), p, table, ws) == (Vec3{0, 0, 0}));
     }
 }
-// test_farfield.cpp:141-168
+// test_farfield.cpp:141-168.  The reference's own errors (measured against its headers,
+// below) halve at every step but one: the Stokeslet error goes 9.6008e-3 -> 5.2967e-3
+// from p = 6 to 8 (ratio 1.81).  The case checks our errors equal the reference's to
+// 1e-6 relative and keeps the >= 2 ratio everywhere the reference meets it.
+static const double kRefDecaySto[6] = {3.772123425498e+00, 4.043395109165e-01, 1.053229570590e-01,
+                                       9.600809639918e-03, 5.296708320533e-03, 8.729388631466e-04};
+static const double kRefDecayStr[6] = {1.530152772136e+00, 5.688418188638e-01, 1.555222529598e-01,
+                                       5.698450605266e-02, 1.559341833953e-02, 4.705758642547e-03};
 static void farfield_geometric_decay() {
     const ParticleSet ps = random_particles(60, 555, true);
     const SingleCluster sc = make_cluster(ps);
@@ -592,8 +609,12 @@ static void farfield_geometric_decay() {
         es[idx] = norm(stokeslet_farfield(dx, m.stokeslet_view(0), p, table, ws) - ex_sto);
         et[idx] = norm(stresslet_farfield(dx, m.stresslet_view(0), p, table, ws) - ex_str);
     }
+    for (int idx = 0; idx < 6; ++idx) {
+        CHECK(rel_diff(es[idx], kRefDecaySto[idx]) < 1e-6);
+        CHECK(rel_diff(et[idx], kRefDecayStr[idx]) < 1e-6);
+    }
     for (int idx = 0; idx + 1 < 6; ++idx) {
-        CHECK(es[idx] / es[idx + 1] >= 2.0);
+        if (idx != 3) CHECK(es[idx] / es[idx + 1] >= 2.0);
         CHECK(et[idx] / et[idx + 1] >= 2.0);
     }
 }
@@ -648,7 +669,10 @@ static void identical_across_runs_and_workers() {
     CHECK(a.stats.farfield_evals == b.stats.farfield_evals);
     CHECK(a.stats.direct_pairs == b.stats.direct_pairs);
 }
-// test_engine.cpp:72-93 ([slow] in the reference)
+// test_engine.cpp:72-93 ([slow] in the reference).  The reference's own e6 is
+// 5.253490138629e-4, just above the case's 5e-4 band (measured against its headers, with
+// e0 = 8.303973923527e-2 and e10 = 3.224066145377e-5); north_star asks E equal to the
+// reference's within 1%, so the band's upper edge becomes that.
 static void sphere_accuracy_bands() {
     const ParticleSet ps = sphere_particles({5, 7});
     CHECK(ps.size() == 20480);
@@ -660,12 +684,14 @@ static void sphere_accuracy_bands() {
     params.order = 6;
     const double e6 = relative_error(direct, treecode_velocity(ps, params).velocity);
     CHECK(e6 >= 5e-6);
-    CHECK(e6 <= 5e-4);
+    CHECK(std::abs(e6 - 5.253490138629e-4) <= 0.01 * 5.253490138629e-4);
     params.order = 0;
     const double e0 = relative_error(direct, treecode_velocity(ps, params).velocity);
     params.order = 10;
     const double e10 = relative_error(direct, treecode_velocity(ps, params).velocity);
     CHECK(e0 / e10 > 1e3);
+    CHECK(std::abs(e0 - 8.303973923527e-2) <= 0.01 * 8.303973923527e-2);
+    CHECK(std::abs(e10 - 3.224066145377e-5) <= 0.01 * 3.224066145377e-5);
 }
 // test_engine.cpp:95-105
 static void high_order_small_theta() {
