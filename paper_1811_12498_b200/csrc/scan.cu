@@ -74,6 +74,32 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_i32(const int32_t* __rest
     if (threadIdx.x == 0) out[nrows] = carry;
 }
 
+// Exclusive scan of nrows uint32 values into uint64 offsets; out[nrows] = total.
+__global__ void __launch_bounds__(kScanThreads) k_scan_u32_u64(const uint32_t* __restrict__ in,
+                                                               uint64_t* __restrict__ out, int nrows) {
+    __shared__ uint64_t warp_sums[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nrows; base += kScanThreads) {
+        const int r = base + threadIdx.x;
+        const uint64_t v = r < nrows ? in[r] : 0u;
+        const uint64_t inc = block_inclusive<uint64_t>(v, warp_sums);
+        const uint64_t cy = carry;
+        if (r < nrows) out[r] = cy + inc - v;
+        __syncthreads();
+        if (threadIdx.x == kScanThreads - 1) carry = cy + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[nrows] = carry;
+}
+
+void launch_scan_u32_u64(const uint32_t* in, uint64_t* out, int nrows, cudaStream_t s) {
+    k_scan_u32_u64<<<1, kScanThreads, 0, s>>>(in, out, nrows);
+    ST_LAUNCH("k_scan_u32_u64");
+    count_launch();
+}
+
 void launch_scan_cols(const uint32_t* in, uint32_t* out, int nrows, int ncols, cudaStream_t s) {
     k_scan_cols<<<1, kScanThreads, 0, s>>>(in, out, nrows, ncols);
     ST_LAUNCH("k_scan_cols");

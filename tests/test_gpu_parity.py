@@ -454,3 +454,17 @@ def test_shard_device_slices_assemble_bit_exactly(S):
     S.unbatch_device(n, torig.data_ptr(), assembled.data_ptr(), out.data_ptr(), stream=stream)
     torch.cuda.synchronize()
     assert torch.equal(out, full)
+
+
+def test_near_field_slabs_are_bit_identical(S, monkeypatch):
+    # the near field's per-entry buffers are cut into slabs of batch warps when they
+    # would not fit; the cut points must not change a single bit
+    ps = S.generate("cube", 30000, 7, True)
+    prm = S.TreecodeParams(order=4, theta=0.5, leaf_capacity=300)
+    a = S.treecode_velocity(ps, prm, per_target=True)
+    for cap in ("5000", "777", "1"):
+        monkeypatch.setenv("ST_NEAR_MAX_ENTRIES", cap)
+        b = S.treecode_velocity(ps, prm, per_target=True)
+        assert np.array_equal(a.velocity, b.velocity)
+        assert np.array_equal(a.per_target, b.per_target)
+        assert b.stats.direct_pairs == a.stats.direct_pairs
