@@ -402,7 +402,8 @@ def run_gpu(args, cfg):
             traffic = None
     ach_near = near_flops / near_s * 1e-12 if world == 1 else None
     ach_far = far_flops / far_s * 1e-12 if world == 1 else None
-    roof = {"bound": "fp64", "kernel": "k_near (near-field leaf direct sum)",
+    roof = {"bound": "fp64",
+            "kernel": "near field: k_neval (leaf direct sums), timed with its k_nwalk plan and k_nreduce",
             "achieved": ach_near, "peak": peak, "unit": "TFLOP/s",
             "frac": (ach_near / peak) if ach_near else None, "traffic": traffic,
             "flops_per_launch": near_flops, "flop_convention": "reference-algorithmic, 48 flop per direct pair",

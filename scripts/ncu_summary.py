@@ -1,7 +1,8 @@
 """Summarise ncu captures for profiles/ (run here, on the .ncu-rep / CSV brought back by gpurun).
 
 python scripts/ncu_summary.py <tag> <launches.csv> <kernel.ncu-rep>... > profiles/<tag>.md
-Also updates profiles/traffic.json with DRAM bytes per launch of k_near / k_far."""
+Also updates profiles/traffic.json with DRAM bytes per launch of the near-field evaluation
+(k_neval) and k_far."""
 import collections
 import csv
 import io
@@ -94,7 +95,7 @@ def main():
                     print(f"| {label} (`{key}`) | {row[i]} {units[i]} |")
             rd = to_bytes(*vals.get("dram__bytes_read.sum", ("0", "byte")))
             wr = to_bytes(*vals.get("dram__bytes_write.sum", ("0", "byte")))
-            kname = "near" if "k_near" in name else "far" if "k_far" in name else name
+            kname = "near" if ("k_near" in name or "k_neval" in name) else "far" if "k_far" in name else name
             traffic.setdefault("cfg1", {})[f"{kname}_dram_bytes_per_launch"] = rd + wr
             print()
     json.dump(traffic, open(traffic_path, "w"), indent=1)
