@@ -221,7 +221,10 @@ def config_block(cfg, args):
             "kernels": "stokeslet+stresslet", "seeds": [SRC_SEED, TGT_SEED] if cfg["targets"] else [SRC_SEED],
             "l2": "flushed between timed steps (512 MiB write, outside the step events)",
             "parallelism": f"targets sharded over {int(os.environ.get('WORLD_SIZE', '1'))} GPU(s), "
-                           "tree+moments replicated"}
+                           "tree+moments replicated" + (
+                               ", shards stored into rank 0's output by the epilogue kernel (CUDA IPC, NVLink)"
+                               if args.gather == "peer" else ", batch-order slices all-gathered over NCCL")
+                           if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "one GPU"}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -232,9 +235,16 @@ def run_gpu(args, cfg):
     import paper_1811_12498_b200 as S
 
     world, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL on the driver's runs; ST_BENCH_BACKEND=gloo lets a one-GPU box smoke-test
+        # the N>1 path (ranks then share the GPU; their kernels never wait on each other)
+        backend = os.environ.get("ST_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
@@ -264,7 +274,16 @@ def run_gpu(args, cfg):
     stride = n * 3 * 8
     ptrs = (base, base + stride, base + 2 * stride, base + 3 * stride)
 
-    if world > 1:
+    peer_out = None
+    if world > 1 and args.gather == "peer":
+        # fused gather: rank 0 exports its output buffer (CUDA IPC); every rank's epilogue
+        # kernel stores its shard's velocities straight into it, in original order, over
+        # NVLink; a one-element NCCL all-reduce after the call orders the ranks
+        obj = [S.ipc_export(dout.data_ptr()) if rank == 0 else None]
+        dist.broadcast_object_list(obj, 0)
+        peer_out = dout.data_ptr() if rank == 0 else S.ipc_open(*obj[0])
+        done = torch.zeros(1, dtype=torch.float32, device=dev)
+    elif world > 1:
         dbatch = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
         torig = torch.empty(nt, dtype=torch.int32, device=dev)
 
@@ -274,6 +293,11 @@ def run_gpu(args, cfg):
         if world == 1:
             return S.treecode_velocity_device(*ptrs, n, prm, dout.data_ptr(), targets_ptr=tp, n_targets=ntp,
                                               stream=sptr)
+        if peer_out is not None:
+            r = S.treecode_velocity_device(*ptrs, n, prm, peer_out, targets_ptr=tp, n_targets=ntp, shard=rank,
+                                           n_shards=world, stream=sptr)
+            dist.all_reduce(done)  # every shard's stores into rank 0's buffer have completed
+            return r
         # every rank: same tree/moments, its work-balanced slice of the Morton-ordered batches in
         # batch order; NCCL all-gather of the slices over NVLink; scatter to original order
         t0, t1, r = S.treecode_shard_device(*ptrs, n, prm, dbatch.data_ptr(), torig.data_ptr(), targets_ptr=tp,
@@ -369,7 +393,8 @@ def run_gpu(args, cfg):
     e2e = {"value": e2e_val, "unit": "targets/s", "h2d_bytes_per_step": int(h2d_bytes) if rank == 0 else 0,
            "d2h_bytes_per_step": int(d2h_bytes),
            "path": "st_treecode_velocity_device with per-step H2D of pinned particle arrays and D2H of the "
-                   "velocities (CUDA events, max over ranks)"}
+                   "velocities (CUDA events, max over ranks)",
+           "step_ms": [round(a.elapsed_time(b), 3) for a, b in ee]}
     if world == 1:
         # the reference-facing host call itself (st_treecode_velocity, engine.hpp:194-196) on
         # pinned host arrays: wall clock around the synchronous call, best of the timed steps
@@ -443,6 +468,9 @@ def run_gpu(args, cfg):
         }
         print(json.dumps(line))
     if world > 1:
+        dist.barrier()
+        if peer_out is not None and rank != 0:
+            S.ipc_close(peer_out)
         dist.destroy_process_group()
 
 
@@ -455,6 +483,9 @@ def main():
     ap.add_argument("--config", default="cfg1", choices=sorted(CONFIGS))
     ap.add_argument("--ref-sample", type=int, default=4000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N>1: shards stored into rank 0's buffer by the epilogue kernel over CUDA IPC "
+                         "(peer), or batch-order slices all-gathered over NCCL and scattered (nccl)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

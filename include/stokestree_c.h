@@ -158,6 +158,18 @@ st_status st_treecode_shard_device(const st_particles* src_device, const double*
 st_status st_unbatch_device(size_t n, const uint32_t* batch_to_original_device,
                             const double* u_batch_device, double* u_out_device, void* stream);
 
+/* ---- one process per GPU: CUDA IPC of an output buffer (NVLink peer stores) ----
+ * st_ipc_export: 64-byte handle of the allocation holding device pointer ptr, and ptr's
+ * offset inside it.  st_ipc_open (in another process, on a GPU with peer access): the
+ * same memory as a device pointer of this process; st_ipc_close releases it.  Passing
+ * the opened pointer as u_out of st_treecode_velocity_device(shard = rank, n_shards =
+ * world) makes every rank's epilogue kernel store its shard's velocities straight into
+ * the owner's buffer in original order: the gather is fused into the kernel (replaces
+ * the reference's per-worker writes into one shared output, engine.hpp:157-169). */
+st_status st_ipc_export(const void* device_ptr, unsigned char handle[64], size_t* offset);
+st_status st_ipc_open(const unsigned char handle[64], size_t offset, void** device_ptr);
+st_status st_ipc_close(void* device_ptr);
+
 /* ---- direct sums (O(N^2) oracle path) ---- */
 /* contracted_direct_velocity(ps, sel, first, last) (kernels.hpp:123-136). */
 st_status st_direct_velocity(const st_particles* src, int stokeslet, int stresslet, size_t first,

@@ -47,6 +47,7 @@ __all__ = [
     "farfield_pairs", "taylor_coeffs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
     "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS", "sphere_particles", "cube_particles",
     "write_particles", "read_particles", "treecode_velocity_sweep",
+    "ipc_export", "ipc_open", "ipc_close",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -62,7 +63,7 @@ EXPORTED_SYMBOLS = (
     "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists", "st_treecode_velocity_sweep",
     "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
     "st_read_particles", "st_loaded_copy", "st_loaded_free", "st_treecode_shard_device", "st_unbatch_device",
-    "st_taylor_coeffs",
+    "st_taylor_coeffs", "st_ipc_export", "st_ipc_open", "st_ipc_close",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -149,6 +150,9 @@ def load_library():
     L.st_treecode_shard_device.argtypes = [P(_Particles), vp, sz, P(_Params), i, i, vp, vp, P(sz), P(sz), vp,
                                            P(_Stats)]
     L.st_unbatch_device.argtypes = [sz, vp, vp, vp, vp]
+    L.st_ipc_export.argtypes = [vp, C.c_char_p, C.POINTER(sz)]
+    L.st_ipc_open.argtypes = [C.c_char_p, sz, C.POINTER(vp)]
+    L.st_ipc_close.argtypes = [vp]
     L.st_sphere_count.restype = sz
     L.st_sphere_count.argtypes = [i]
     L.st_generate_sphere_icosa.argtypes = [i, C.c_uint64, vp, vp, vp, vp]
@@ -363,6 +367,29 @@ def treecode_shard_device(position_ptr, force_ptr, dipole_ptr, normal_ptr, n, pa
 
 def unbatch_device(n, batch_to_original_ptr, u_batch_ptr, u_out_ptr, stream=0):
     _check(load_library().st_unbatch_device(n, batch_to_original_ptr, u_batch_ptr, u_out_ptr, stream))
+
+
+def ipc_export(device_ptr: int):
+    """(64-byte CUDA IPC handle, offset) of the allocation holding ``device_ptr``; another
+    process opens it with ipc_open and can pass the result as ``u_out_ptr`` of
+    treecode_velocity_device(shard=rank, n_shards=world): its epilogue then stores the
+    shard straight into this buffer (NVLink peer stores, no gather)."""
+    h = C.create_string_buffer(64)
+    off = C.c_size_t(0)
+    _check(load_library().st_ipc_export(device_ptr, h, C.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    if len(handle) != 64:
+        raise InvalidArgument("ipc_open: a CUDA IPC handle is 64 bytes")
+    p = C.c_void_p(0)
+    _check(load_library().st_ipc_open(handle, offset, C.byref(p)))
+    return p.value
+
+
+def ipc_close(device_ptr: int) -> None:
+    _check(load_library().st_ipc_close(device_ptr))
 
 
 def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],

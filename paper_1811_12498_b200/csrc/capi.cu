@@ -1,8 +1,11 @@
 // C ABI of libstokestree_b200.so (include/stokestree_c.h): validation with the
 // reference's error taxonomy and messages, device buffer management, and the
 // orchestration of K1 (tree) -> K2 (moments + fold) -> K3/K4 (far) -> K5 (near).
+#include <cuda.h>
+
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -543,10 +546,11 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
 
 // Replicated-data multi-GPU in one process (PAPER.md:986-1030 with GPUs for MPI ranks):
 // one host thread per logical device uploads the inputs, rebuilds the (bit-identical)
-// tree and moments, evaluates its work-balanced shard of the Morton-ordered batches in
-// batch order and peer-copies that contiguous slice (NVLink P2P) into device 0, which
-// scatters the gathered batch-order velocities to original order.  Logical devices
-// beyond the physical count share GPUs round-robin (same results, no speedup).
+// tree and moments and evaluates its work-balanced shard of the Morton-ordered batches.
+// The shard's epilogue (k_nreduce, and the count walk for per-target statistics) stores
+// straight into device 0's output in original order -- NVLink peer stores from the
+// kernel, no gather or scatter pass.  Logical devices beyond the physical count share
+// GPUs round-robin (same results, no speedup).
 void multi_device(const st_particles* src, const double* targets, size_t n_targets, const st_params& prm,
                   double* u_out, uint64_t* per_target, RunOut& ro_all, double& t_h2d, double& t_d2h) {
     const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
@@ -556,14 +560,25 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
     const size_t nt = targets ? n_targets : src->n;
     int dev0 = 0;
     ST_CUDA(cudaGetDevice(&dev0));
+    for (int d = 1; d < std::min(D, ndev); ++d) {  // peer stores into device 0
+        const int dev = (dev0 + d) % ndev;
+        int can = 0;
+        ST_CUDA(cudaDeviceCanAccessPeer(&can, dev, dev0));
+        if (!can) fail(ST_CUDA_ERROR, "devices > 1: GPU " + std::to_string(dev) + " cannot access GPU " +
+                                          std::to_string(dev0) + " (NVLink peer access required)");
+        ST_CUDA(cudaSetDevice(dev));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dev0, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+    }
+    ST_CUDA(cudaSetDevice(dev0));
     OwnedStream os0;
     cudaStream_t s0 = os0.s;
-    DevArray<double> gath(3 * nt, s0);
-    DevArray<uint64_t> gpt(per_target ? 3 * nt : 0, s0);
-    ST_CUDA(cudaStreamSynchronize(s0));  // allocations complete before other devices copy into them
+    DevArray<double> du(3 * nt, s0);
+    DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s0);
+    ST_CUDA(cudaStreamSynchronize(s0));  // allocations complete before other devices store into them
     std::vector<RunOut> ros(D);
     std::vector<std::exception_ptr> errs(D);
-    ShardOut so0;
     auto work = [&](int d) {
         try {
             const int dev = (dev0 + d) % ndev;
@@ -578,28 +593,9 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
                 dt.alloc(3 * nt, s);
                 ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
             }
-            if (d == 0) {
-                run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, gath.get(), per_target ? gpt.get() : nullptr,
-                             0, D, s, ros[0], true, &so0);
-                ST_CUDA(cudaStreamSynchronize(s));
-                raise_flags(ros[0]);
-                return;
-            }
-            DevArray<double> du(3 * nt, s);
-            DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s);
-            ShardOut so;
             run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d, D,
-                         s, ros[d], true, &so);
+                         s, ros[d]);
             raise_flags(ros[d]);
-            const size_t t0 = (size_t)so.w0 * 32, t1 = std::min(nt, (size_t)so.w1 * 32);
-            if (t1 > t0) {
-                ST_CUDA(cudaMemcpyPeerAsync(gath.get() + 3 * t0, dev0, du.get() + 3 * t0, dev,
-                                            3 * (t1 - t0) * sizeof(double), s));
-                if (per_target)
-                    ST_CUDA(cudaMemcpyPeerAsync(gpt.get() + 3 * t0, dev0, dpt.get() + 3 * t0, dev,
-                                                3 * (t1 - t0) * sizeof(uint64_t), s));
-            }
-            ST_CUDA(cudaStreamSynchronize(s));
         } catch (...) {
             errs[d] = std::current_exception();
         }
@@ -607,17 +603,11 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
     std::vector<std::thread> th;
     for (int d = 1; d < D; ++d) th.emplace_back(work, d);
     work(0);
-    for (auto& t : th) t.join();
+    for (auto& t : th) t.join();  // every shard's stream has completed (run_treecode synchronises)
     ST_CUDA(cudaSetDevice(dev0));
     for (auto& e : errs)
         if (e) std::rethrow_exception(e);
     Event d0, d1;
-    DevArray<double> du(3 * nt, s0);
-    DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s0);
-    k_unbatch<<<nblocks(nt, 256), 256, 0, s0>>>(nt, so0.torig.get(), gath.get(), gpt.get(), du.get(),
-                                                per_target ? dpt.get() : nullptr);
-    ST_LAUNCH("k_unbatch");
-    count_launch();
     d0.record(s0);
     ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s0));
     if (per_target)
@@ -831,6 +821,63 @@ st_status st_unbatch_device(size_t n, const uint32_t* batch_to_original, const d
         k_unbatch<<<nblocks(n, 256), 256, 0, s>>>(n, batch_to_original, u_batch, nullptr, u_out, nullptr);
         ST_LAUNCH("k_unbatch");
         count_launch();
+    });
+}
+
+namespace {
+std::mutex g_ipc_mu;
+std::map<void*, void*> g_ipc_open;  // pointer handed out by st_ipc_open -> mapped allocation base
+}  // namespace
+
+st_status st_ipc_export(const void* dptr, unsigned char handle[64], size_t* offset) {
+    return guarded([&] {
+        if (!dptr || !handle || !offset) fail(ST_INVALID_ARGUMENT, "ipc_export: null pointer");
+        ensure_device();
+        using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static GetRange get_range = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            ST_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+            if (!fn || q != cudaDriverEntryPointSuccess) fail(ST_CUDA_ERROR, "ipc_export: cuMemGetAddressRange missing");
+            return reinterpret_cast<GetRange>(fn);
+        }();
+        CUdeviceptr base = 0;
+        size_t bytes = 0;
+        if (get_range(&base, &bytes, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS)
+            fail(ST_INVALID_ARGUMENT, "ipc_export: not a device allocation");
+        cudaIpcMemHandle_t h;
+        ST_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+        static_assert(sizeof h == 64, "CUDA IPC handles are 64 bytes");
+        std::memcpy(handle, &h, sizeof h);
+        *offset = static_cast<size_t>(reinterpret_cast<CUdeviceptr>(dptr) - base);
+    });
+}
+
+st_status st_ipc_open(const unsigned char handle[64], size_t offset, void** dptr) {
+    return guarded([&] {
+        if (!handle || !dptr) fail(ST_INVALID_ARGUMENT, "ipc_open: null pointer");
+        ensure_device();
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        void* base = nullptr;
+        ST_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        *dptr = static_cast<char*>(base) + offset;
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        g_ipc_open[*dptr] = base;
+    });
+}
+
+st_status st_ipc_close(void* dptr) {
+    return guarded([&] {
+        void* base = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_ipc_mu);
+            auto it = g_ipc_open.find(dptr);
+            if (it == g_ipc_open.end()) fail(ST_INVALID_ARGUMENT, "ipc_close: pointer not from st_ipc_open");
+            base = it->second;
+            g_ipc_open.erase(it);
+        }
+        ST_CUDA(cudaIpcCloseMemHandle(base));
     });
 }
 

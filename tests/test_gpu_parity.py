@@ -468,3 +468,21 @@ def test_near_field_slabs_are_bit_identical(S, monkeypatch):
         assert np.array_equal(a.velocity, b.velocity)
         assert np.array_equal(a.per_target, b.per_target)
         assert b.stats.direct_pairs == a.stats.direct_pairs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_fused_gather(world):
+    # bench.py's N>1 path: every rank's epilogue stores its shard into rank 0's buffer
+    # through CUDA IPC (ranks share the one GPU here; they never wait on each other)
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(here, "ipc_worker.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
