@@ -8,12 +8,14 @@
 #include <map>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "moments.cuh"
+#include "staging.cuh"
 #include "traverse.cuh"
 #include "tree.cuh"
 
@@ -257,7 +259,7 @@ void upload(const st_particles* ps, bool need_f, bool need_hn, DevParticles& d, 
     auto up = [&](const double* src, DevArray<double>& dst) -> const double* {
         if (!src) return nullptr;
         dst.alloc(3 * ps->n, s);
-        ST_CUDA(cudaMemcpyAsync(dst.get(), src, 3 * ps->n * sizeof(double), cudaMemcpyHostToDevice, s));
+        h2d(dst.get(), src, 3 * ps->n * sizeof(double), s);
         return dst.get();
     };
     d.pos = up(ps->position, d.own_pos);
@@ -591,7 +593,7 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
             DevArray<double> dt;
             if (targets) {
                 dt.alloc(3 * nt, s);
-                ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
+                h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
             }
             run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d, D,
                          s, ros[d]);
@@ -609,9 +611,8 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
         if (e) std::rethrow_exception(e);
     Event d0, d1;
     d0.record(s0);
-    ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s0));
-    if (per_target)
-        ST_CUDA(cudaMemcpyAsync(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), cudaMemcpyDeviceToHost, s0));
+    d2h(u_out, du.get(), 3 * nt * sizeof(double), s0);
+    if (per_target) d2h(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), s0);
     d1.record(s0);
     ST_CUDA(cudaStreamSynchronize(s0));
     t_d2h = secs(d0, d1);
@@ -699,7 +700,7 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
         auto up = [&](const double* hsrc, DevArray<double>& dst, cudaStream_t st) -> const double* {
             if (!hsrc) return nullptr;
             dst.alloc(3 * src->n, st);
-            ST_CUDA(cudaMemcpyAsync(dst.get(), hsrc, 3 * src->n * sizeof(double), cudaMemcpyHostToDevice, st));
+            h2d(dst.get(), hsrc, 3 * src->n * sizeof(double), st);
             return dst.get();
         };
         d.pos = up(src->position, d.own_pos, s);
@@ -707,7 +708,7 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
         DevArray<double> dt;
         if (targets) {
             dt.alloc(3 * nt, s);
-            ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
+            h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
         }
         d.f = sto ? up(src->force_weight, d.own_f, s2) : nullptr;
         d.h = str ? up(src->dipole_weight, d.own_h, s2) : nullptr;
@@ -720,9 +721,8 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
                      1, s, ro, false, nullptr, wready.e);
         raise_flags(ro);
         d0.record(s);
-        ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (per_target)
-            ST_CUDA(cudaMemcpyAsync(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        d2h(u_out, du.get(), 3 * nt * sizeof(double), s);
+        if (per_target) d2h(per_target, dpt.get(), 3 * nt * sizeof(uint64_t), s);
         d1.record(s);
         ST_CUDA(cudaStreamSynchronize(s));
         // stream-ordered frees of the s2 uploads must not race the compute stream
@@ -758,13 +758,13 @@ st_status st_treecode_velocity_sweep(const st_particles* src, const double* targ
         DevArray<double> dt;
         if (targets) {
             dt.alloc(3 * nt, s);
-            ST_CUDA(cudaMemcpyAsync(dt.get(), targets, 3 * nt * sizeof(double), cudaMemcpyHostToDevice, s));
+            h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
         }
         DevArray<double> du(3 * nt * (size_t)n_orders, s);
         RunOut ro;
         run_sweep(d, targets ? dt.get() : nullptr, nt, *params, orders, n_orders, du.get(), far_seconds, s, ro);
         raise_flags(ro);
-        ST_CUDA(cudaMemcpyAsync(u_out, du.get(), du.bytes(), cudaMemcpyDeviceToHost, s));
+        d2h(u_out, du.get(), du.bytes(), s);
         ST_CUDA(cudaStreamSynchronize(s));
         fill_stats(stats, ro);
         if (stats) stats->gpu_launches = g_launches;
@@ -984,7 +984,7 @@ static void direct_common(const st_particles* src, int sto, int str, const std::
     }
     int herr = 0;
     ST_CUDA(cudaMemcpyAsync(&herr, err.get(), sizeof herr, cudaMemcpyDeviceToHost, s));
-    if (nt) ST_CUDA(cudaMemcpyAsync(u_out, du.get(), 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (nt) d2h(u_out, du.get(), 3 * nt * sizeof(double), s);
     ST_CUDA(cudaStreamSynchronize(s));
     if (herr)
         fail(ST_DOMAIN_ERROR, naive ? "stokeslet: coincident points" : "direct sum: coincident particles");

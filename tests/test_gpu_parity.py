@@ -486,3 +486,21 @@ def test_ipc_fused_gather(world):
                         "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(here, "ipc_worker.py")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_pageable_and_pinned_inputs_agree(S):
+    # pageable host arrays go through the pinned staging ring in 4 MB chunks (an odd size
+    # here: 3 full chunks + a tail per array); pinned arrays are copied directly
+    import torch
+    n = 175_001
+    ps = S.generate("cube", n, 21, True)
+    prm = S.TreecodeParams(order=3, theta=0.6, leaf_capacity=1000)
+    a = S.treecode_velocity(ps, prm)
+    pin = torch.empty((4 * n, 3), dtype=torch.float64).pin_memory().numpy()
+    pin[:] = np.concatenate([ps.position, ps.force_weight, ps.dipole_weight, ps.normal])
+    pps = S.ParticleSet(pin[:n], pin[n:2 * n], pin[2 * n:3 * n], pin[3 * n:])
+    b = S.treecode_velocity(pps, prm)
+    assert np.array_equal(a.velocity, b.velocity)
+    d = S.contracted_direct_velocity_at(ps, S.KernelSelection.both(), np.arange(0, n, 997))
+    e = S.contracted_direct_velocity_at(pps, S.KernelSelection.both(), np.arange(0, n, 997))
+    assert np.array_equal(d, e)
