@@ -522,10 +522,14 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
     for (int d = (int)lv.size() - 1; d >= 0; --d) {
         const int cnt = (int)lv[d].size();
         if (!cnt) continue;
+        // one CTA per parent and few parents per level: as many threads as the launch
+        // bound allows (the fewest entries per thread), unlike the leaf kernel
+        const int mept = (E + kThreads - 1) / kThreads <= 1 ? 1 : (E + kThreads - 1) / kThreads <= 2 ? 2 : 4;
+        const int mthreads = std::max(32, ((E + mept - 1) / mept + 31) / 32 * 32);
         auto go = [&](auto kern) {
             ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<cnt, threads, smem, s>>>(d_lvl.get() + lvl_off[d], tree.children.get(), tree.nchild.get(),
-                                            tree.geom.get(), p, E, M.get());
+            kern<<<cnt, mthreads, smem, s>>>(d_lvl.get() + lvl_off[d], tree.children.get(), tree.nchild.get(),
+                                             tree.geom.get(), p, E, M.get());
             ST_LAUNCH("k_m2m");
             count_launch();
         };
@@ -535,8 +539,8 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
             else if (sto) go(k_m2m<EP, true, false>);
             else go(k_m2m<EP, false, true>);
         };
-        if (ept == 1) pick(std::integral_constant<int, 1>{});
-        else if (ept == 2) pick(std::integral_constant<int, 2>{});
+        if (mept == 1) pick(std::integral_constant<int, 1>{});
+        else if (mept == 2) pick(std::integral_constant<int, 2>{});
         else pick(std::integral_constant<int, 4>{});
     }
     stamp("m2m");
