@@ -63,7 +63,7 @@ def dist_env():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled in-process through NVML (pynvml) every 200 ms
+    """SM clocks + throttle reasons sampled in-process through NVML (pynvml) every 25 ms
     during the timed region (lighter than an nvidia-smi subprocess next to the step)."""
 
     def __init__(self, gpu_index):
@@ -95,7 +95,7 @@ class ClockSampler:
                 self.lines.append((time.time(), sm, mx, rs))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.025)
 
     def wait_first(self, timeout=5.0):
         t0 = time.time()
@@ -111,8 +111,8 @@ class ClockSampler:
             self.t.join(timeout=2)
 
     def summary(self):
-        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
-                "sw_power_cap": 0x4}
+        bits = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
         sm, mx, reasons = [], None, set()
         for ts, f, m, rs in self.lines:
             if not (self.window[0] - 0.1 <= ts <= self.window[1] + 0.1):
@@ -124,8 +124,8 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0, "source": "nvml"}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml (pynvml), 200 ms"}
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(np.min(sm)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml (pynvml), 25 ms"}
 
 
 def allgather_batch_slices(dist, ubatch, t0, t1, world):

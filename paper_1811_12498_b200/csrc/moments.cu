@@ -165,7 +165,10 @@ __global__ void __launch_bounds__(kThreads)
 
 // M2M (exact algebra): the moments of a cluster about its centre c_p from its children's
 // moments about theirs, M_p[k] = sum_children sum_{j<=k} C(k,j) (c_c - c_p)^(k-j) M_c[j]
-// (componentwise binomials).  Children in slot order, j in a fixed order: deterministic.
+// (componentwise binomials).  The shift is separable, so it runs as three 1-D passes
+// (z, then y, then x) through shared memory: every entry costs at most p+1 terms per pass
+// instead of prod(k_a+1) (up to 80 at p = 10), which balanced the threads of a CTA.
+// Children in slot order, fixed term order: deterministic.
 template <int EPT, bool STO, bool STR>
 __global__ void __launch_bounds__(kThreads)
     k_m2m(const int32_t* __restrict__ ids, const int32_t* __restrict__ children,
@@ -174,8 +177,9 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int NC = (STO ? 3 : 0) + (STR ? 9 : 0);
     constexpr int C0 = STO ? 0 : 3;
     extern __shared__ __align__(16) double m2m_smem[];
-    double* Mc = m2m_smem;                         // [E][12] child moments
-    double* A = m2m_smem + (size_t)E * 12;         // [3][p+1][p+1]: C(k,j) d^(k-j)
+    double* Ma = m2m_smem;                         // [E][12] child moments / y-pass output
+    double* Mb = m2m_smem + (size_t)E * 12;        // [E][12] z-pass output
+    double* A = m2m_smem + (size_t)E * 24;         // [3][p+1][p+1]: C(k,j) d^(k-j)
     const int T = blockDim.x;
     const int v = ids[blockIdx.x];
     const double4 gp = geom[v];
@@ -192,11 +196,38 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int c = 0; c < NC; ++c) acc[j][c] = 0.0;
     const int P1 = p + 1;
+    // one 1-D pass along axis `ax`: out[k] = sum_{j_ax <= k_ax} A[ax][k_ax][j_ax] in[k with j_ax]
+    auto pass = [&](int ax, const double* in, double* out, bool accumulate) {
+#pragma unroll
+        for (int jj = 0; jj < EPT; ++jj) {
+            const int e = threadIdx.x + jj * T;
+            if (e >= E) continue;
+            int q[3] = {kk[jj][0], kk[jj][1], kk[jj][2]};
+            const int ka = q[ax];
+            double t[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) t[c] = 0.0;
+            for (int j = 0; j <= ka; ++j) {
+                q[ax] = j;
+                const double cf = A[(ax * P1 + ka) * P1 + j];
+                const double* mj = in + (size_t)mi_flat(q[0], q[1], q[2]) * 12 + C0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) t[c] = fma(cf, mj[c], t[c]);
+            }
+            if (accumulate) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) acc[jj][c] += t[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) out[(size_t)e * 12 + C0 + c] = t[c];
+            }
+        }
+    };
     for (int ch = 0; ch < nchild[v]; ++ch) {
         const int u = children[8 * v + ch];
         const double4 gc = geom[u];
-        __syncthreads();
-        for (int x = threadIdx.x; x < E * 12; x += T) Mc[x] = M[(size_t)u * E * 12 + x];
+        __syncthreads();  // the previous child's passes are done with Ma, A
+        for (int x = threadIdx.x; x < E * 12; x += T) Ma[x] = M[(size_t)u * E * 12 + x];
         for (int x = threadIdx.x; x < 3 * P1 * P1; x += T) {
             const int a = x / (P1 * P1), k = (x / P1) % P1, j = x % P1;
             const double d = a == 0 ? gc.x - gp.x : a == 1 ? gc.y - gp.y : gc.z - gp.z;
@@ -212,24 +243,11 @@ __global__ void __launch_bounds__(kThreads)
             A[x] = c;
         }
         __syncthreads();
-#pragma unroll
-        for (int jj = 0; jj < EPT; ++jj) {
-            const int e = threadIdx.x + jj * T;
-            if (e >= E) continue;
-            const int k1 = kk[jj][0], k2 = kk[jj][1], k3 = kk[jj][2];
-            for (int j1 = 0; j1 <= k1; ++j1) {
-                const double a1 = A[(0 * P1 + k1) * P1 + j1];
-                for (int j2 = 0; j2 <= k2; ++j2) {
-                    const double a12 = a1 * A[(1 * P1 + k2) * P1 + j2];
-                    for (int j3 = 0; j3 <= k3; ++j3) {
-                        const double cf = a12 * A[(2 * P1 + k3) * P1 + j3];
-                        const double* mj = Mc + (size_t)mi_flat(j1, j2, j3) * 12 + C0;
-#pragma unroll
-                        for (int c = 0; c < NC; ++c) acc[jj][c] = fma(cf, mj[c], acc[jj][c]);
-                    }
-                }
-            }
-        }
+        pass(2, Ma, Mb, false);
+        __syncthreads();
+        pass(1, Mb, Ma, false);
+        __syncthreads();
+        pass(0, Ma, nullptr, true);
     }
 #pragma unroll
     for (int jj = 0; jj < EPT; ++jj) {
@@ -512,7 +530,7 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
     }
     stamp("leaves");
     // upward pass: deepest internal level first
-    const size_t smem = sizeof(double) * ((size_t)E * 12 + 3 * (size_t)(p + 1) * (p + 1));
+    const size_t smem = sizeof(double) * ((size_t)E * 24 + 3 * (size_t)(p + 1) * (p + 1));
     size_t base = 0;
     std::vector<size_t> lvl_off;
     for (const auto& ids : lv) {
