@@ -51,7 +51,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libstokestree_b200.so")
+# ST_LIB_PATH: load another build of the library (A/B checks of kernel changes)
+lib_path = os.environ.get("ST_LIB_PATH") or os.path.join(_HERE, "libstokestree_b200.so")
 
 # every symbol declared in include/stokestree_c.h
 EXPORTED_SYMBOLS = (
