@@ -504,3 +504,31 @@ def test_pageable_and_pinned_inputs_agree(S):
     d = S.contracted_direct_velocity_at(ps, S.KernelSelection.both(), np.arange(0, n, 997))
     e = S.contracted_direct_velocity_at(pps, S.KernelSelection.both(), np.arange(0, n, 997))
     assert np.array_equal(d, e)
+
+
+def test_concurrent_calls_from_host_threads(S):
+    # ctypes releases the GIL: four host threads call the library at once on one device
+    # (shared per-device workspace, staging rings, copy pool); each result must equal the
+    # sequential one bit for bit
+    import threading
+    cases = [(S.generate("cube", 60000 + 7000 * i, 50 + i, True),
+              S.TreecodeParams(order=3 + i, theta=0.5, leaf_capacity=400)) for i in range(4)]
+    want = [S.treecode_velocity(ps, prm).velocity for ps, prm in cases]
+    got = [None] * 4
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                got[i] = S.treecode_velocity(*cases[i]).velocity
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)
