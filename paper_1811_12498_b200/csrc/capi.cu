@@ -342,13 +342,13 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     M.reset();
     e2.record(s);
 
-    // batch order of the targets: a leaf-capacity-32 octree over the target points
+    // batch order of the targets: 63-bit Morton order in their tight box (one radix sort)
     const double* tpos = same ? src.pos : d_targets;
-    DevTree ttree;
-    build_tree_device(tpos, nt, 32, false, false, s, ttree);
+    DevArray<uint32_t> tperm;
+    order_targets(tpos, nt, s, tperm);
     DevArray<double> tx(3 * nt, s), ufar(3 * nt, s);
     DevArray<uint32_t> torig(nt, s), tskip(nt, s);
-    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, ttree.perm.get(), tpos, same ? to_tree.get() : nullptr,
+    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr,
                                                tx.get(), torig.get(), tskip.get());
     ST_LAUNCH("k_targets");
     count_launch();
@@ -489,11 +489,11 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     compute_moments_device(tree, rec.get(), pmax, sto, str, s, M);
     e2.record(s);
     const double* tpos = same ? src.pos : d_targets;
-    DevTree ttree;
-    build_tree_device(tpos, nt, 32, false, false, s, ttree);
+    DevArray<uint32_t> tperm;
+    order_targets(tpos, nt, s, tperm);
     DevArray<double> tx(3 * nt, s), ufar(3 * nt, s), unear(3 * nt, s);
     DevArray<uint32_t> torig(nt, s), tskip(nt, s);
-    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, ttree.perm.get(), tpos, same ? to_tree.get() : nullptr, tx.get(),
+    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr, tx.get(),
                                                torig.get(), tskip.get());
     ST_LAUNCH("k_targets");
     count_launch();

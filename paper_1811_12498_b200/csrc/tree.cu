@@ -18,6 +18,8 @@
 #include "scan.cuh"
 #include "tree.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace st {
 
 namespace {
@@ -84,6 +86,36 @@ __global__ void k_tight_all(const double* __restrict__ pos, size_t n,
             atomicMax(&mm[3 + a], (unsigned long long)hi[a]);
         }
     }
+}
+
+// 63-bit Morton key (21 bits per axis) of each point inside the tight box: the order of
+// the target batches (any spatially coherent order serves; results do not depend on it)
+__device__ __forceinline__ uint64_t spread21(uint64_t v) {
+    v &= 0x1fffffull;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+__global__ void k_morton(const double* __restrict__ pos, size_t n, const unsigned long long* __restrict__ mm,
+                         uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double lo[3], side = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = ord_dec(mm[a]);
+        side = fmax(side, ord_dec(mm[3 + a]) - lo[a]);
+    }
+    const double inv = side > 0.0 ? 2097151.0 / side : 0.0;
+    uint64_t k = 0;
+    for (int a = 0; a < 3; ++a) {
+        const double q = fmin(fmax((pos[3 * i + a] - lo[a]) * inv, 0.0), 2097151.0);
+        k |= spread21((uint64_t)q) << (2 - a);
+    }
+    key[i] = k;
+    idx[i] = (uint32_t)i;
 }
 
 // Root cube (cluster_tree.hpp:163-169): side = max extent * (1 + 1e-12), centred
@@ -646,6 +678,28 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     ST_LAUNCH("k_finalize");
     count_launch();
     out.perm = std::move(perm);
+}
+
+void order_targets(const double* d_pos, size_t n, cudaStream_t s, DevArray<uint32_t>& perm) {
+    perm.alloc(n, s);
+    if (!n) return;
+    DevArray<unsigned long long> mm(6, s);
+    const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+    ST_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof init, cudaMemcpyHostToDevice, s));
+    const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
+    k_tight_all<<<g, 256, 0, s>>>(d_pos, n, mm.get());
+    ST_LAUNCH("k_tight_all");
+    DevArray<uint64_t> key(n, s), key2(n, s);
+    DevArray<uint32_t> idx(n, s);
+    k_morton<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d_pos, n, mm.get(), key.get(), idx.get());
+    ST_LAUNCH("k_morton");
+    size_t tmp = 0;
+    ST_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), key2.get(), idx.get(), perm.get(), (int)n, 0,
+                                            63, s));
+    DevArray<char> scratch(tmp, s);
+    ST_CUDA(cub::DeviceRadixSort::SortPairs(scratch.get(), tmp, key.get(), key2.get(), idx.get(), perm.get(), (int)n,
+                                            0, 63, s));
+    count_launch(3);
 }
 
 }  // namespace st

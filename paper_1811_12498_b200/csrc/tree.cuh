@@ -27,4 +27,8 @@ struct DevTree {
 void build_tree_device(const double* d_pos, size_t n, int n0, bool shrink, bool geometry,
                        cudaStream_t s, DevTree& out);
 
+// Order of n points (device, xyz) by 63-bit Morton key in their tight box: perm[i] is the
+// original index of the i-th point.  Stream-ordered, no host synchronisation.
+void order_targets(const double* d_pos, size_t n, cudaStream_t s, DevArray<uint32_t>& perm);
+
 }  // namespace st
