@@ -398,10 +398,15 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         a.warp_cost = nullptr;
     }
 
+    // the far kernel's walk also counts the near field's entries (no separate count walk)
+    NearCounts nc;
+    nc.attach(a, s);
+    a.count = 1;
     ef0.record(s);
     launch_far(P, a, s);
     ef1.record(s);
-    launch_near(sto, str, a, s);
+    a.count = 0;
+    launch_near(sto, str, a, s, &nc);
     en1.record(s);
     e3.record(s);
 
@@ -501,7 +506,6 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     DevArray<int> d_err(1, s), d_work(2, s);
     d_stats.zero();
     d_err.zero();
-    ufar.zero();
     TravArgs a;
     a.tx = tx.get();
     a.tskip = tskip.get();
@@ -514,21 +518,31 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     a.ncl = tree.ncl;
     a.th2 = prm.theta * prm.theta;
     a.src = rec.get();
-    a.ufar = ufar.get();  // zeros: the near pass stores near-field sums only
-    a.out = unear.get();
     a.stats = d_stats.get();
     a.err = d_err.get();
     a.work = d_work.get();
-    launch_near(sto, str, a, s);
+    DevArray<double> zeros(3 * nt, s);
+    zeros.zero();
+    NearCounts nc;
     for (int i = 0; i < n_orders; ++i) {
         Event f0, f1;
         DevArray<double> W;
         fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, s, W, pmax);
         a.W = W.get();
+        a.ufar = ufar.get();
         a.out = nullptr;
+        if (i == 0) nc.attach(a, s);  // the first far pass also counts the near field's entries
+        a.count = i == 0;
         f0.record(s);
         launch_far(orders[i] + (str ? 2 : 1), a, s);
         f1.record(s);
+        a.count = 0;
+        if (i == 0) {  // ONE near pass (independent of the order): near sums only (far input zero)
+            TravArgs an = a;
+            an.ufar = zeros.get();
+            an.out = unear.get();
+            launch_near(sto, str, an, s, &nc);
+        }
         k_combine<<<nblocks(nt, 256), 256, 0, s>>>(nt, torig.get(), ufar.get(), unear.get(), d_out + 3 * nt * i);
         ST_LAUNCH("k_combine");
         count_launch();

@@ -27,12 +27,36 @@ struct TravArgs {
     float* warp_cost = nullptr;      // count pass: per-warp work estimate
     int out_batch = 0;               // 1: write out / per_target in batch order (slot t), not torig[t]
     int* work = nullptr;             // persistent kernels: next batch counter (zeroed per launch)
+    // k_far with count = 1 also does the near plan's counting pass (the same DFS): near
+    // leaves per target, near entries per batch warp (index warp - w0) and per source leaf,
+    // and the statistics (stats, per_target)
+    int count = 0;
+    uint32_t* cnt_kn = nullptr;      // [nt]
+    uint32_t* cnt_wcnt = nullptr;    // [w1 - w0]
+    int32_t* cnt_leaf = nullptr;     // [ncl], zeroed by the caller
+};
+
+// Storage for the counting pass shared by k_far and the near field (see TravArgs::count).
+struct NearCounts {
+    DevArray<uint32_t> kn, wcnt;
+    DevArray<int32_t> leaf;
+    // allocate for a's warp range, zero the leaf counts, and point a's cnt_* fields at them
+    void attach(TravArgs& a, cudaStream_t s) {
+        kn.alloc(a.nt, s);
+        wcnt.alloc(a.w1 - a.w0, s);
+        leaf.alloc(a.ncl, s);
+        leaf.zero();
+        a.cnt_kn = kn.get();
+        a.cnt_wcnt = wcnt.get();
+        a.cnt_leaf = leaf.get();
+    }
 };
 
 // Far field for warps [w0, w1): P = p + 2 (stresslet) or p + 1.
 void launch_far(int P, const TravArgs& a, cudaStream_t s);
-// Near field + combine + scatter to original order + counters.
-void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s);
+// Near field + combine + scatter to original order + counters.  With counts (filled by
+// a counting k_far over the same warp range) the near field skips its own counting walk.
+void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s, const NearCounts* counts = nullptr);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
