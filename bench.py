@@ -205,7 +205,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "targets/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": nt / value * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64)",
         "config": config_block(cfg, args),
         "cpu_baseline": {"value": value, "unit": "targets/s", "cores": threads, "kind": "reference",
                          "sample": desc},
