@@ -77,6 +77,22 @@ void ensure_device() {
             if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
                 uint64_t thr = UINT64_MAX;
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                // Map a block of pool memory once and keep it: a stream-ordered allocation
+                // that has to grow the pool was measured to block the host for 10-550 ms
+                // (GB-size requests at cfg4), mid-call.  8% of the device (ST_POOL_RESERVE_GB
+                // overrides); larger problems still grow the pool as needed.
+                size_t fr = 0, tot = 0;
+                if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+                    size_t reserve = tot / 100 * 8;
+                    if (const char* env = getenv("ST_POOL_RESERVE_GB")) reserve = (size_t)(atof(env) * 1e9);
+                    reserve = std::min(reserve, fr / 2);
+                    void* p = nullptr;
+                    if (reserve && cudaMallocAsync(&p, reserve, 0) == cudaSuccess) {
+                        cudaFreeAsync(p, 0);
+                        cudaStreamSynchronize(0);
+                    }
+                    cudaGetLastError();
+                }
             }
         } else {
             fail(ST_CUDA_ERROR, "device " + std::to_string(dev) + " is sm_" + std::to_string(major) +

@@ -3,6 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cstddef>
 #include <cstdint>
 #include <stdexcept>
@@ -56,7 +60,15 @@ public:
         reset();
         stream_ = s;
         n_ = n;
-        if (n) ST_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+        if (n) {
+            static const bool dbg = getenv("ST_DEBUG_ALLOC") != nullptr;
+            const auto t0 = std::chrono::steady_clock::now();
+            ST_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+            if (dbg) {
+                const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                if (ms > 1.0) fprintf(stderr, "[alloc] %.1f MB took %.1f ms\n", n * sizeof(T) / 1e6, ms);
+            }
+        }
     }
     void reset() {
         if (p_) cudaFreeAsync(p_, stream_);
