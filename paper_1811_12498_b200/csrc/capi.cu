@@ -157,15 +157,6 @@ __global__ void k_targets(size_t nt, const uint32_t* __restrict__ tperm, const d
     tskip[t] = to_tree ? to_tree[o] : kNoSkip;
 }
 
-// sweep: u_p = far_p + near for every target (same summation as the single-order path)
-__global__ void k_combine(size_t nt, const uint32_t* __restrict__ torig, const double* __restrict__ ufar,
-                          const double* __restrict__ unear, double* __restrict__ u) {
-    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (t >= nt) return;
-    const size_t o = torig[t];
-    for (int a = 0; a < 3; ++a) u[3 * o + a] = ufar[3 * t + a] + unear[3 * o + a];
-}
-
 // batch order -> original order (multi-device gather on device 0)
 __global__ void k_unbatch(size_t nt, const uint32_t* __restrict__ torig, const double* __restrict__ ub,
                           const uint64_t* __restrict__ pb, double* __restrict__ u, uint64_t* __restrict__ pt) {
@@ -305,6 +296,17 @@ void raise_flags(const RunOut& ro) {
 }
 
 
+// Far events (clusters) accepted by at most this many of a warp's 32 lanes are not
+// evaluated by k_far, which would idle the other lanes, but packed 32 per task by the near
+// field's plan: 24 measured best (cfg1 -2%, cfg4 -6%); ST_FAR_SPARSE overrides, 0 disables.
+int far_sparse_max() {
+    static const int v = [] {
+        const char* e = getenv("ST_FAR_SPARSE");
+        return e ? std::max(0, std::min(31, atoi(e))) : 24;
+    }();
+    return v;
+}
+
 void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
 
 struct ShardOut {
@@ -414,7 +416,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         a.warp_cost = nullptr;
     }
 
-    // the far kernel's walk also counts the near field's entries (no separate count walk)
+    // the far kernel's walk also counts the near field's entries (no separate count walk),
+    // and leaves sparse far events to the near field's packed far pass
+    a.sparse_max = far_sparse_max();
+    a.P = P;
     NearCounts nc;
     nc.attach(a, s);
     a.count = 1;
@@ -512,7 +517,7 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     const double* tpos = same ? src.pos : d_targets;
     DevArray<uint32_t> tperm;
     order_targets(tpos, nt, s, tperm);
-    DevArray<double> tx(3 * nt, s), ufar(3 * nt, s), unear(3 * nt, s);
+    DevArray<double> tx(3 * nt, s);
     DevArray<uint32_t> torig(nt, s), tskip(nt, s);
     k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr, tx.get(),
                                                torig.get(), tskip.get());
@@ -537,34 +542,36 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     a.stats = d_stats.get();
     a.err = d_err.get();
     a.work = d_work.get();
-    DevArray<double> zeros(3 * nt, s);
-    zeros.zero();
+    // per order: the fold and the dense far field (the first pass also counts the near
+    // field's entries); then ONE near pass combined with every order (deferred sparse far
+    // events evaluated per order with its weights): each order is bit-identical to a
+    // standalone call at that order
+    a.sparse_max = far_sparse_max();
     NearCounts nc;
+    std::vector<DevArray<double>> Ws(n_orders), ufars(n_orders);
+    std::vector<FarOrder> fo(n_orders);
     for (int i = 0; i < n_orders; ++i) {
         Event f0, f1;
-        DevArray<double> W;
-        fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, s, W, pmax);
-        a.W = W.get();
-        a.ufar = ufar.get();
+        fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, s, Ws[i], pmax);
+        ufars[i].alloc(3 * nt, s);
+        a.W = Ws[i].get();
+        a.P = orders[i] + (str ? 2 : 1);
+        a.ufar = ufars[i].get();
         a.out = nullptr;
-        if (i == 0) nc.attach(a, s);  // the first far pass also counts the near field's entries
+        if (i == 0) nc.attach(a, s);
         a.count = i == 0;
         f0.record(s);
-        launch_far(orders[i] + (str ? 2 : 1), a, s);
+        launch_far(a.P, a, s);
         f1.record(s);
         a.count = 0;
-        if (i == 0) {  // ONE near pass (independent of the order): near sums only (far input zero)
-            TravArgs an = a;
-            an.ufar = zeros.get();
-            an.out = unear.get();
-            launch_near(sto, str, an, s, &nc);
-        }
-        k_combine<<<nblocks(nt, 256), 256, 0, s>>>(nt, torig.get(), ufar.get(), unear.get(), d_out + 3 * nt * i);
-        ST_LAUNCH("k_combine");
-        count_launch();
         ST_CUDA(cudaStreamSynchronize(s));
         if (far_s) far_s[i] = secs(f0, f1);
+        fo[i].P = a.P;
+        fo[i].W = Ws[i].get();
+        fo[i].ufar = ufars[i].get();
+        fo[i].out = d_out + 3 * nt * i;
     }
+    launch_near(sto, str, a, s, &nc, fo.data(), n_orders);
     e3.record(s);
     ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaMemcpyAsync(ro.stats, d_stats.get(), sizeof ro.stats, cudaMemcpyDeviceToHost, s));

@@ -34,29 +34,58 @@ struct TravArgs {
     uint32_t* cnt_kn = nullptr;      // [nt]
     uint32_t* cnt_wcnt = nullptr;    // [w1 - w0]
     int32_t* cnt_leaf = nullptr;     // [ncl], zeroed by the caller
+    // Sparse far events: k_far does not evaluate a cluster accepted by <= sparse_max lanes
+    // of the warp (it would idle the other lanes); when counting it counts those entries
+    // (per target, per batch warp, per cluster) and the near field's plan evaluates them
+    // packed 32 per task (needs W and P).  0 disables deferral.
+    int sparse_max = 0;
+    int P = 0;                       // far order of W
+    uint32_t* cnt_kd = nullptr;      // [nt]
+    uint32_t* cnt_wd = nullptr;      // [w1 - w0]
+    int32_t* cnt_dcl = nullptr;      // [ncl], zeroed by the caller
 };
 
 // Storage for the counting pass shared by k_far and the near field (see TravArgs::count).
 struct NearCounts {
-    DevArray<uint32_t> kn, wcnt;
-    DevArray<int32_t> leaf;
-    // allocate for a's warp range, zero the leaf counts, and point a's cnt_* fields at them
+    DevArray<uint32_t> kn, wcnt, kd, wd;
+    DevArray<int32_t> leaf, dcl;
+    int sparse_max = 0;              // the deferral threshold the counting k_far used
+    // allocate for a's warp range, zero the bucket counts, and point a's cnt_* fields at them
     void attach(TravArgs& a, cudaStream_t s) {
         kn.alloc(a.nt, s);
         wcnt.alloc(a.w1 - a.w0, s);
         leaf.alloc(a.ncl, s);
         leaf.zero();
+        kd.alloc(a.nt, s);
+        wd.alloc(a.w1 - a.w0, s);
+        dcl.alloc(a.ncl, s);
+        dcl.zero();
         a.cnt_kn = kn.get();
         a.cnt_wcnt = wcnt.get();
         a.cnt_leaf = leaf.get();
+        a.cnt_kd = kd.get();
+        a.cnt_wd = wd.get();
+        a.cnt_dcl = dcl.get();
+        sparse_max = a.sparse_max;
     }
 };
 
 // Far field for warps [w0, w1): P = p + 2 (stresslet) or p + 1.
 void launch_far(int P, const TravArgs& a, cudaStream_t s);
-// Near field + combine + scatter to original order + counters.  With counts (filled by
-// a counting k_far over the same warp range) the near field skips its own counting walk.
-void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s, const NearCounts* counts = nullptr);
+// One far order to combine with the near field: its weights (for the deferred sparse
+// events), the dense far sums k_far wrote, and the output.
+struct FarOrder {
+    int P = 0;
+    const double* W = nullptr;
+    const double* ufar = nullptr;
+    double* out = nullptr;
+};
+// Near field + deferred far events + combine + scatter to original order + counters.  With
+// counts (filled by a counting k_far over the same warp range) the near field skips its
+// own counting walk.  Orders: the near sums are formed once and combined with each order
+// (default: the single order described by a.P, a.W, a.ufar, a.out).
+void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s, const NearCounts* counts = nullptr,
+                 const FarOrder* orders = nullptr, int n_orders = 0);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
