@@ -436,12 +436,13 @@ def run_gpu(args, cfg):
     ach_near = near_flops / near_s * 1e-12 if world == 1 else None
     ach_far = far_flops / far_s * 1e-12 if world == 1 else None
     roof = {"bound": "fp64",
-            "kernel": "near field: k_neval (leaf direct sums), timed with its k_nwalk plan and k_nreduce",
+            "kernel": "k_neval (near-field leaf direct sums; CUDA events around its launches)",
             "achieved": ach_near, "peak": peak, "unit": "TFLOP/s",
             "frac": (ach_near / peak) if ach_near else None, "traffic": traffic,
             "flops_per_launch": near_flops, "flop_convention": "reference-algorithmic, 48 flop per direct pair",
             "peak_source": "live DFMA-loop probe in this run (MEASURED_PEAKS.json has no FP64 figure)",
-            "far": {"kernel": "k_far (MAC traversal + Taylor far field)", "achieved": ach_far,
+            "far": {"kernel": "k_far (MAC walk + dense far events) + k_feval (sparse far events, packed)",
+                    "achieved": ach_far,
                     "frac": (ach_far / peak) if ach_far else None, "flops_per_launch": far_flops,
                     "flop_convention": f"reference-algorithmic (reference-equivalent), {f_far(cfg['order'])} "
                                        "flop per accepted pair; executed flops are ~15x fewer (harmonic "

@@ -110,19 +110,6 @@ struct OwnedStream {
     }
 };
 
-struct Event {
-    cudaEvent_t e = nullptr;
-    Event() { ST_CUDA(cudaEventCreate(&e)); }
-    ~Event() {
-        if (e) cudaEventDestroy(e);
-    }
-    void record(cudaStream_t s) { ST_CUDA(cudaEventRecord(e, s)); }
-};
-double secs(const Event& a, const Event& b) {
-    float ms = 0.f;
-    ST_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
-    return ms * 1e-3;
-}
 
 inline unsigned nblocks(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
@@ -427,7 +414,8 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     launch_far(P, a, s);
     ef1.record(s);
     a.count = 0;
-    launch_near(sto, str, a, s, &nc);
+    NearTimes nt_times;
+    launch_near(sto, str, a, s, &nc, nullptr, 0, &nt_times);
     en1.record(s);
     e3.record(s);
 
@@ -439,8 +427,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ro.t_moments = secs(e1, e2);
     ro.t_traverse = secs(e2, e3);
     ro.t_total = secs(e0, e3);
-    ro.t_far = secs(ef0, ef1);
-    ro.t_near = secs(ef1, en1);
+    // kernel times: far = dense events (k_far) + deferred sparse events (k_feval); near =
+    // the leaf sums (k_neval).  Walks, scans and the reduce count in t_traverse only.
+    ro.t_far = secs(ef0, ef1) + nt_times.far_deferred_s;
+    ro.t_near = nt_times.near_eval_s;
     if (so) {
         so->w0 = a.w0;
         so->w1 = a.w1;

@@ -37,6 +37,24 @@ inline void cuda_check(cudaError_t e, const char* what) {
 extern thread_local uint64_t g_launches;
 inline void count_launch(uint64_t k = 1) { g_launches += k; }
 
+// Timing event (move-only; destroyed with its owner).
+struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { ST_CUDA(cudaEventCreate(&e)); }
+    Event(const Event&) = delete;
+    Event& operator=(const Event&) = delete;
+    Event(Event&& o) noexcept : e(o.e) { o.e = nullptr; }
+    ~Event() {
+        if (e) cudaEventDestroy(e);
+    }
+    void record(cudaStream_t s) { ST_CUDA(cudaEventRecord(e, s)); }
+};
+inline double secs(const Event& a, const Event& b) {
+    float ms = 0.f;
+    ST_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
+    return ms * 1e-3;
+}
+
 // Stream-ordered device array (cudaMallocAsync on the device's default pool,
 // whose release threshold is raised once so memory is recycled across calls).
 template <class T>

@@ -84,8 +84,12 @@ struct FarOrder {
 // counts (filled by a counting k_far over the same warp range) the near field skips its
 // own counting walk.  Orders: the near sums are formed once and combined with each order
 // (default: the single order described by a.P, a.W, a.ufar, a.out).
+struct NearTimes {
+    double near_eval_s = 0.0;        // k_neval (all slabs)
+    double far_deferred_s = 0.0;     // k_feval over the deferred sparse far events (all orders)
+};
 void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s, const NearCounts* counts = nullptr,
-                 const FarOrder* orders = nullptr, int n_orders = 0);
+                 const FarOrder* orders = nullptr, int n_orders = 0, NearTimes* times = nullptr);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
