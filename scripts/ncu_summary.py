@@ -95,7 +95,8 @@ def main():
                     print(f"| {label} (`{key}`) | {row[i]} {units[i]} |")
             rd = to_bytes(*vals.get("dram__bytes_read.sum", ("0", "byte")))
             wr = to_bytes(*vals.get("dram__bytes_write.sum", ("0", "byte")))
-            kname = "near" if ("k_near" in name or "k_neval" in name) else "far" if "k_far" in name else name
+            kname = ("near" if ("k_near" in name or "k_neval" in name) else "far_deferred" if "k_feval" in name
+                     else "far" if "k_far" in name else name)
             traffic.setdefault("cfg1", {})[f"{kname}_dram_bytes_per_launch"] = rd + wr
             print()
     json.dump(traffic, open(traffic_path, "w"), indent=1)
