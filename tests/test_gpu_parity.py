@@ -532,3 +532,29 @@ def test_concurrent_calls_from_host_threads(S):
     assert not errs, errs
     for w, g in zip(want, got):
         assert np.array_equal(w, g)
+
+
+def test_far_deferral_changes_rounding_only(S, need_ref, tmp_path):
+    # sparse far events (accepted by <= 24 of a warp's lanes) are evaluated by the packed
+    # pass and added after the dense ones; with ST_FAR_SPARSE=0 k_far evaluates every event.
+    # Both orders agree to rounding and both match the reference treecode.
+    import os
+    import subprocess
+    import sys
+    ps = S.generate("mixture", 40000, 19, True)
+    prm = S.TreecodeParams(order=6, theta=0.6, leaf_capacity=300)
+    a = S.treecode_velocity(ps, prm).velocity
+    out = tmp_path / "u0.npy"
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1811_12498_b200 as S; "
+            "ps = S.generate('mixture', 40000, 19, True); "
+            "prm = S.TreecodeParams(order=6, theta=0.6, leaf_capacity=300); "
+            "np.save(%r, S.treecode_velocity(ps, prm).velocity)" % (os.path.dirname(os.path.dirname(
+                os.path.abspath(__file__))), str(out)))
+    env = dict(os.environ, ST_FAR_SPARSE="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    b = np.load(out)
+    assert S.relative_error(b, a) <= 1e-14
+    ctx = need_ref.RefContext(as_dict(ps), 6, 0.6, 300, True)
+    u_ref, _, _ = ctx.eval(src_idx=np.arange(ps.size()), threads=8)
+    assert S.relative_error(u_ref, a) <= REL_TOL and S.relative_error(u_ref, b) <= REL_TOL
