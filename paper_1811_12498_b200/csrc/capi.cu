@@ -390,11 +390,16 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         // work-balanced contiguous warp ranges, identical on every rank (deterministic)
         DevArray<float> cost(nwarps, s);
         a.warp_cost = cost.get();
-        const float cf = (float)((P + 1) * (P + 1) * 10), cn = 32.f;
+        // a dense far event costs ~8 (P+1)^2 warp DP instructions; a near (lane, source)
+        // pair ~1 (30 per 32 lanes)
+        a.sparse_max = far_sparse_max();
+        const float cf = (float)((P + 1) * (P + 1) * 8), cn = 1.f;
         launch_count(a, cf, cn, s);
         std::vector<float> hc(nwarps);
         ST_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), sizeof(float) * nwarps, cudaMemcpyDeviceToHost, s));
         ST_CUDA(cudaStreamSynchronize(s));
+        for (int w = 0; w < nwarps; ++w)  // every kCountStride-th warp was sampled
+            if (w % kCountStride) hc[w] = hc[w - w % kCountStride];
         std::vector<double> w(hc.begin(), hc.end());
         std::vector<size_t> cuts(nshards + 1);
         shard_cuts_host(nwarps, w.data(), nshards, cuts.data());

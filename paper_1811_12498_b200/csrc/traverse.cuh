@@ -93,7 +93,9 @@ void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s, const Ne
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
-// Traversal-only work estimate per warp (for multi-GPU shard cuts).
+// Traversal-only work estimate of every 4th warp of [a.w0, a.w1) into a.warp_cost (for
+// multi-GPU shard cuts; the caller fills the warps in between from the preceding sample).
+constexpr int kCountStride = 4;
 void launch_count(const TravArgs& a, float far_cost, float near_cost, cudaStream_t s);
 
 // O(N^2) contracted direct sum (kernels.hpp:45-83, 123-150): sources are the
