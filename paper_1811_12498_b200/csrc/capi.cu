@@ -314,7 +314,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     const bool same = d_targets == nullptr;
     const size_t nt = same ? n : nt_in;
     if (nt >= 0x7fffffffull - 64) fail(ST_INVALID_ARGUMENT, "too many targets");
-    Event e0, e1, e2, e3, ef0, ef1, en1;
+    Event e0, e1, e2, e3;
     e0.record(s);
 
     // K1: tree over the sources, tree-ordered source records
@@ -375,9 +375,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     a.info = tree.info.get();
     a.ncl = tree.ncl;
     a.th2 = prm.theta * prm.theta;
-    a.W = W.get();
     a.src = rec.get();
-    a.ufar = ufar.get();
     a.out = d_out;
     a.per_target = d_per_target;
     a.stats = d_stats.get();
@@ -408,20 +406,14 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         a.warp_cost = nullptr;
     }
 
-    // the far kernel's walk also counts the near field's entries (no separate count walk),
-    // and leaves sparse far events to the near field's packed far pass
     a.sparse_max = far_sparse_max();
-    a.P = P;
-    NearCounts nc;
-    nc.attach(a, s);
-    a.count = 1;
-    ef0.record(s);
-    launch_far(P, a, s);
-    ef1.record(s);
-    a.count = 0;
-    NearTimes nt_times;
-    launch_near(sto, str, a, s, &nc, nullptr, 0, &nt_times);
-    en1.record(s);
+    FarOrder fo;
+    fo.P = P;
+    fo.W = W.get();
+    fo.ufar = ufar.get();
+    fo.out = d_out;
+    EvalTimes tm;
+    launch_eval(sto, str, a, &fo, 1, s, &tm);
     e3.record(s);
 
     ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -432,10 +424,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ro.t_moments = secs(e1, e2);
     ro.t_traverse = secs(e2, e3);
     ro.t_total = secs(e0, e3);
-    // kernel times: far = dense events (k_far) + deferred sparse events (k_feval); near =
-    // the leaf sums (k_neval).  Walks, scans and the reduce count in t_traverse only.
-    ro.t_far = secs(ef0, ef1) + nt_times.far_deferred_s;
-    ro.t_near = nt_times.near_eval_s;
+    // kernel times: far = dense events (k_far_list) + deferred sparse events (k_feval);
+    // near = the leaf sums (k_neval).  Walks, scans and the reduce count in t_traverse only.
+    ro.t_far = tm.far_s;
+    ro.t_near = tm.near_s;
     if (so) {
         so->w0 = a.w0;
         so->w1 = a.w1;
@@ -537,36 +529,23 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     a.stats = d_stats.get();
     a.err = d_err.get();
     a.work = d_work.get();
-    // per order: the fold and the dense far field (the first pass also counts the near
-    // field's entries); then ONE near pass combined with every order (deferred sparse far
-    // events evaluated per order with its weights): each order is bit-identical to a
-    // standalone call at that order
+    // one plan, one near-field pass; per order the fold, the dense far events, the packed
+    // sparse ones and the reduce: each order is bit-identical to a standalone call
     a.sparse_max = far_sparse_max();
-    NearCounts nc;
     std::vector<DevArray<double>> Ws(n_orders), ufars(n_orders);
     std::vector<FarOrder> fo(n_orders);
     for (int i = 0; i < n_orders; ++i) {
-        Event f0, f1;
         fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, s, Ws[i], pmax);
         ufars[i].alloc(3 * nt, s);
-        a.W = Ws[i].get();
-        a.P = orders[i] + (str ? 2 : 1);
-        a.ufar = ufars[i].get();
-        a.out = nullptr;
-        if (i == 0) nc.attach(a, s);
-        a.count = i == 0;
-        f0.record(s);
-        launch_far(a.P, a, s);
-        f1.record(s);
-        a.count = 0;
-        ST_CUDA(cudaStreamSynchronize(s));
-        if (far_s) far_s[i] = secs(f0, f1);
-        fo[i].P = a.P;
+        fo[i].P = orders[i] + (str ? 2 : 1);
         fo[i].W = Ws[i].get();
         fo[i].ufar = ufars[i].get();
         fo[i].out = d_out + 3 * nt * i;
     }
-    launch_near(sto, str, a, s, &nc, fo.data(), n_orders);
+    EvalTimes tm;
+    launch_eval(sto, str, a, fo.data(), n_orders, s, &tm);
+    for (int i = 0; i < n_orders; ++i)
+        if (far_s) far_s[i] = tm.far_order[i];
     e3.record(s);
     ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaMemcpyAsync(ro.stats, d_stats.get(), sizeof ro.stats, cudaMemcpyDeviceToHost, s));

@@ -1,6 +1,8 @@
 // K3-K6: MAC traversal, far field, near field, O(N^2) direct sums.
 #pragma once
 
+#include <vector>
+
 #include "st_common.cuh"
 
 namespace st {
@@ -17,9 +19,7 @@ struct TravArgs {
     const int4* info = nullptr;      // begin, end, next, is_leaf
     int ncl = 0;
     double th2 = 0.0;                // theta * theta
-    const double* W = nullptr;       // far weights [ncl][(P+1)^2][4]
     const double* src = nullptr;     // tree-ordered source records [n][12]
-    double* ufar = nullptr;          // far-field sums per batch position [nt][3]
     double* out = nullptr;           // final velocities, original target order [nt][3]
     uint64_t* per_target = nullptr;  // optional {visited, far, direct}, original order
     unsigned long long* stats = nullptr;  // {farfield_evals, direct_pairs, clusters_visited}
@@ -27,69 +27,31 @@ struct TravArgs {
     float* warp_cost = nullptr;      // count pass: per-warp work estimate
     int out_batch = 0;               // 1: write out / per_target in batch order (slot t), not torig[t]
     int* work = nullptr;             // persistent kernels: next batch counter (zeroed per launch)
-    // k_far with count = 1 also does the near plan's counting pass (the same DFS): near
-    // leaves per target, near entries per batch warp (index warp - w0) and per source leaf,
-    // and the statistics (stats, per_target)
-    int count = 0;
-    uint32_t* cnt_kn = nullptr;      // [nt]
-    uint32_t* cnt_wcnt = nullptr;    // [w1 - w0]
-    int32_t* cnt_leaf = nullptr;     // [ncl], zeroed by the caller
-    // Sparse far events: k_far does not evaluate a cluster accepted by <= sparse_max lanes
-    // of the warp (it would idle the other lanes); when counting it counts those entries
-    // (per target, per batch warp, per cluster) and the near field's plan evaluates them
-    // packed 32 per task (needs W and P).  0 disables deferral.
+    // far events accepted by <= sparse_max lanes of a warp are evaluated by the packed
+    // pass (k_feval) instead of the warp's event list (k_far_list); 0 disables
     int sparse_max = 0;
-    int P = 0;                       // far order of W
-    uint32_t* cnt_kd = nullptr;      // [nt]
-    uint32_t* cnt_wd = nullptr;      // [w1 - w0]
-    int32_t* cnt_dcl = nullptr;      // [ncl], zeroed by the caller
 };
 
-// Storage for the counting pass shared by k_far and the near field (see TravArgs::count).
-struct NearCounts {
-    DevArray<uint32_t> kn, wcnt, kd, wd;
-    DevArray<int32_t> leaf, dcl;
-    int sparse_max = 0;              // the deferral threshold the counting k_far used
-    // allocate for a's warp range, zero the bucket counts, and point a's cnt_* fields at them
-    void attach(TravArgs& a, cudaStream_t s) {
-        kn.alloc(a.nt, s);
-        wcnt.alloc(a.w1 - a.w0, s);
-        leaf.alloc(a.ncl, s);
-        leaf.zero();
-        kd.alloc(a.nt, s);
-        wd.alloc(a.w1 - a.w0, s);
-        dcl.alloc(a.ncl, s);
-        dcl.zero();
-        a.cnt_kn = kn.get();
-        a.cnt_wcnt = wcnt.get();
-        a.cnt_leaf = leaf.get();
-        a.cnt_kd = kd.get();
-        a.cnt_wd = wd.get();
-        a.cnt_dcl = dcl.get();
-        sparse_max = a.sparse_max;
-    }
-};
-
-// Far field for warps [w0, w1): P = p + 2 (stresslet) or p + 1.
-void launch_far(int P, const TravArgs& a, cudaStream_t s);
-// One far order to combine with the near field: its weights (for the deferred sparse
-// events), the dense far sums k_far wrote, and the output.
+// One far order: its folded weights (P = p + 2 with stresslets, else p + 1), a buffer for
+// the dense far sums (nt x 3, batch order) and the output.
 struct FarOrder {
     int P = 0;
     const double* W = nullptr;
-    const double* ufar = nullptr;
+    double* ufar = nullptr;
     double* out = nullptr;
 };
-// Near field + deferred far events + combine + scatter to original order + counters.  With
-// counts (filled by a counting k_far over the same warp range) the near field skips its
-// own counting walk.  Orders: the near sums are formed once and combined with each order
-// (default: the single order described by a.P, a.W, a.ufar, a.out).
-struct NearTimes {
-    double near_eval_s = 0.0;        // k_neval (all slabs)
-    double far_deferred_s = 0.0;     // k_feval over the deferred sparse far events (all orders)
+struct EvalTimes {
+    double near_s = 0.0;            // k_neval (all slabs)
+    double far_s = 0.0;             // k_far_list + k_feval (all slabs and orders)
+    std::vector<double> far_order;  // the same per order
 };
-void launch_near(bool sto, bool str, const TravArgs& a, cudaStream_t s, const NearCounts* counts = nullptr,
-                 const FarOrder* orders = nullptr, int n_orders = 0, NearTimes* times = nullptr);
+// K3-K5 for the batch warps [a.w0, a.w1): the plan walks (counts, then near entries,
+// deferred sparse far entries and each warp's dense far events), then per slab the dense
+// far field of every order, the near field once, the packed sparse far events and the
+// reduce per order (original order unless a.out_batch); counters into a.stats and
+// a.per_target.  Synchronises the stream before returning.
+void launch_eval(bool sto, bool str, const TravArgs& a, const FarOrder* orders, int n_orders, cudaStream_t s,
+                 EvalTimes* times = nullptr);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
