@@ -79,12 +79,24 @@ __global__ void k_tight_all(const double* __restrict__ pos, size_t n,
         lo[a] = warp_min(lo[a]);
         hi[a] = warp_max(hi[a]);
     }
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
+    // one atomic per block and value (per-warp atomics on 6 addresses serialised)
+    __shared__ uint64_t s_lo[32][3], s_hi[32][3];
+    const int wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0)
         for (int a = 0; a < 3; ++a) {
-            atomicMin(&mm[a], (unsigned long long)lo[a]);
-            atomicMax(&mm[3 + a], (unsigned long long)hi[a]);
+            s_lo[wid][a] = lo[a];
+            s_hi[wid][a] = hi[a];
         }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x;
+        uint64_t l = ~0ull, h = 0;
+        for (int w = 0; w < nw; ++w) {
+            l = s_lo[w][a] < l ? s_lo[w][a] : l;
+            h = h < s_hi[w][a] ? s_hi[w][a] : h;
+        }
+        atomicMin(&mm[a], (unsigned long long)l);
+        atomicMax(&mm[3 + a], (unsigned long long)h);
     }
 }
 
