@@ -558,3 +558,19 @@ def test_far_deferral_changes_rounding_only(S, need_ref, tmp_path):
     ctx = need_ref.RefContext(as_dict(ps), 6, 0.6, 300, True)
     u_ref, _, _ = ctx.eval(src_idx=np.arange(ps.size()), threads=8)
     assert S.relative_error(u_ref, a) <= REL_TOL and S.relative_error(u_ref, b) <= REL_TOL
+
+
+@pytest.mark.parametrize("n,n0,order,theta,sel", [
+    (2, 1, 3, 0.5, "both"), (31, 1, 2, 0.9, "both"), (33, 2, 4, 0.5, "stokeslet_only"),
+    (95, 3, 6, 0.7, "stresslet_only"), (257, 1, 1, 0.8, "both"), (1000, 7, 8, 0.4, "both"),
+])
+def test_ragged_sizes_match_reference(S, need_ref, n, n0, order, theta, sel):
+    # batch boundaries (32 targets), one-particle leaves, every kernel selection: the
+    # planned evaluation (near entries, dense far lists, deferred sparse far events)
+    ksel = getattr(S.KernelSelection, sel)()
+    ps = S.generate("unit", n, 1000 + n, ksel.stresslet_enabled)
+    res, u_ref, pt_ref, st_ref = run_pair(S, need_ref, ps, order, theta, n0, sel=ksel)
+    assert np.array_equal(res.per_target, pt_ref)
+    assert res.stats.farfield_evals == st_ref["farfield_evals"]
+    assert res.stats.direct_pairs == st_ref["direct_pairs"]
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
