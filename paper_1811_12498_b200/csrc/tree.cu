@@ -589,24 +589,30 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         ST_LAUNCH("k_nch");
         launch_scan_i32(nch.get(), chbase.get(), m, s);
         count_launch(6);
-        const int C = read_i32(chbase.get() + m, s);
-
-        const size_t need = (size_t)total + C;
+        // sized by the bound C <= 8m so the children are made without waiting for C; one
+        // host round trip per level reads C and the next level's split count together
+        const int Cmax = 8 * m;
+        const size_t need = (size_t)total + Cmax;
         grow(nb_begin, need, total, s);
         grow(nb_end, need, total, s);
         grow(nb_first, need, total, s);
         grow(nb_nch, need, total, s);
         grow(nb_box, 6 * need, 6 * (size_t)total, s);
 
-        DevArray<int32_t> flag(C, s), fpos(C + 1, s);
+        DevArray<int32_t> flag(Cmax, s), fpos(Cmax + 1, s);
+        ST_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t) * Cmax, s));
         k_children<<<blocks(m, 128), 128, 0, s>>>(m, act.get(), seg_begin.get(), seg_cnt.get(),
                                                   chbase.get(), total, n0, depth + 1, nb_box.get(),
                                                   nb_box.get(), nb_begin.get(), nb_end.get(),
                                                   nb_first.get(), nb_nch.get(), flag.get());
         ST_LAUNCH("k_children");
-        launch_scan_i32(flag.get(), fpos.get(), C, s);
+        launch_scan_i32(flag.get(), fpos.get(), Cmax, s);
         count_launch();
-        const int m2 = read_i32(fpos.get() + C, s);
+        int32_t cm[2] = {0, 0};  // C, next level's split count
+        ST_CUDA(cudaMemcpyAsync(&cm[0], chbase.get() + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaMemcpyAsync(&cm[1], fpos.get() + Cmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        const int C = cm[0], m2 = cm[1];
         DevArray<int32_t> act2(std::max(m2, 1), s);
         if (m2) {
             k_compact<<<blocks(C, 256), 256, 0, s>>>(C, total, flag.get(), fpos.get(), act2.get());
