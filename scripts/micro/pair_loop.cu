@@ -70,6 +70,61 @@ __global__ void kpair(double* out, int iters) {
     for (int v = 0; v < 2 && v < U; ++v) s += u[v][0] + u[v][1] + u[v][2];
     if (s == 1.2345 || bad) out[0] = s;
 }
+// two targets per lane share each record's shared-memory loads
+__device__ __forceinline__ void pair2(const double* r, double x0, double x1, double x2, double z0, double z1,
+                                      double z2, double* u, double* w) {
+    const double2 p01 = *reinterpret_cast<const double2*>(r);
+    const double2 p2f0 = *reinterpret_cast<const double2*>(r + 2);
+    const double2 f12 = *reinterpret_cast<const double2*>(r + 4);
+    const double2 h01 = *reinterpret_cast<const double2*>(r + 6);
+    const double2 h2n0 = *reinterpret_cast<const double2*>(r + 8);
+    const double2 n12 = *reinterpret_cast<const double2*>(r + 10);
+    const double f0 = p2f0.y, f1 = f12.x, f2 = f12.y;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double a0 = k ? z0 : x0, a1 = k ? z1 : x1, a2 = k ? z2 : x2;
+        double* acc = k ? w : u;
+        const double d0 = a0 - p01.x, d1 = a1 - p01.y, d2 = a2 - p2f0.x;
+        const double rr = fma(d2, d2, fma(d1, d1, d0 * d0));
+        const double rinv = rsqrt_dp(rr);
+        const double rinv2 = rinv * rinv;
+        const double df = fma(d2, f2, fma(d1, f1, d0 * f0));
+        const double dh = fma(d2, h2n0.x, fma(d1, h01.y, d0 * h01.x));
+        const double dn = fma(d2, n12.y, fma(d1, n12.x, d0 * h2n0.y));
+        const double sc = fma(dh * dn, rinv2, df) * rinv2;
+        acc[0] = fma(rinv, fma(d0, sc, f0), acc[0]);
+        acc[1] = fma(rinv, fma(d1, sc, f1), acc[1]);
+        acc[2] = fma(rinv, fma(d2, sc, f2), acc[2]);
+    }
+}
+template <int U>
+__global__ void kpair2(double* out, int iters) {
+    __shared__ __align__(16) double rec[64 * 12];
+    for (int i = threadIdx.x; i < 64 * 12; i += blockDim.x) rec[i] = 0.1 + 0.01 * (i % 12) + 0.001 * (i / 12);
+    __syncthreads();
+    const double x0 = 1.0 + threadIdx.x * 1e-3, x1 = 2.0, x2 = 3.0, z0 = 1.5 + threadIdx.x * 1e-3, z1 = 2.5, z2 = 3.5;
+    double u[2][3] = {}, w[2][3] = {};
+    for (int it = 0; it < iters; ++it)
+        for (int q = 0; q < 64; q += U)
+#pragma unroll
+            for (int v = 0; v < U; ++v) pair2(rec + 12 * (q + v), x0, x1, x2, z0, z1, z2, u[v & 1], w[v & 1]);
+    double s = u[0][0] + u[1][1] + u[0][2] + w[0][0] + w[1][1] + w[1][2];
+    if (s == 1.2345) out[0] = s;
+}
+template <int U>
+void run2(int threads, int blocks_per_sm, int iters) {
+    int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    double* o; cudaMalloc(&o, 8);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    const int grid = nsm * blocks_per_sm;
+    kpair2<U><<<grid, threads>>>(o, 2);
+    cudaEventRecord(e0);
+    kpair2<U><<<grid, threads>>>(o, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    const double pairs = (double)grid * threads * iters * 64 * 2;
+    printf("2tgt    U=%d warps/SM=%2d: %.3e pairs/s\n", U, threads / 32 * blocks_per_sm, pairs / (ms * 1e-3));
+}
 template <int U, int F32 = 0>
 void run(int threads, int blocks_per_sm, int iters) {
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -88,8 +143,8 @@ void run(int threads, int blocks_per_sm, int iters) {
 int main() {
     for (int wps : {16, 24, 32}) {
         run<4>(256, wps / 8, 400);
-        run<4, 1>(256, wps / 8, 400);
-        run<4, 2>(256, wps / 8, 400);
+        run2<2>(256, wps / 8, 200);
+        run2<4>(256, wps / 8, 200);
     }
     return 0;
 }
