@@ -72,12 +72,21 @@ def main():
           "(sm_100a), one launch per kernel, BASELINE cfg1 (N=1M cube, p=8, theta=0.5, N0=2000). "
           "ncu times are cold-cache and serialised: compare shares, not absolutes.\n")
     tot, cnt = launches(lcsv)
-    T = sum(tot.values())
-    print("## Launch list (`--metrics gpu__time_duration.sum`), one treecode step\n")
-    print("| kernel | launches | ms | share |\n|---|---|---|---|")
+    # a bench.py launch list also holds its live FP64 peak probe (not part of a step) and
+    # warm-up + timed steps: report per step, counting steps by near-field launches
+    probe = [k for k in tot if "fp64_peak" in k]
+    for k in probe:
+        tot.pop(k)
+        cnt.pop(k)
+    steps = max([c for k, c in cnt.items() if k.startswith("st::k_neval")] or [1])
+    T = sum(tot.values()) / steps
+    title = "one treecode step" if steps == 1 else f"per treecode step (list of {steps} steps" + \
+        (", FP64 peak probe excluded)" if probe else ")")
+    print(f"## Launch list (`--metrics gpu__time_duration.sum`), {title}\n")
+    print("| kernel | launches/step | ms/step | share |\n|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda x: -x[1])[:14]:
-        print(f"| `{k}` | {cnt[k]} | {v:.3f} | {100 * v / T:.1f}% |")
-    print(f"| total | {sum(cnt.values())} | {T:.3f} | |\n")
+        print(f"| `{k}` | {cnt[k] / steps:g} | {v / steps:.3f} | {100 * v / steps / T:.1f}% |")
+    print(f"| total | {sum(cnt.values()) / steps:g} | {T:.3f} | |\n")
     traffic_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for rep in reps:
