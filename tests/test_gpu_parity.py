@@ -574,3 +574,19 @@ def test_ragged_sizes_match_reference(S, need_ref, n, n0, order, theta, sel):
     assert res.stats.farfield_evals == st_ref["farfield_evals"]
     assert res.stats.direct_pairs == st_ref["direct_pairs"]
     assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
+def test_near_plan_invariants_debug_checker():
+    """ST_DEBUG_NEAR runs the bucket invariant kernels (every entry once, holes only in self
+    regions, self entries at their record position) on self and disjoint targets, one slab
+    and many, all three kernel selections; slab results must be bit-identical."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ST_DEBUG_NEAR="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "sanitize_near.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("ok: slabs bit-identical") == 3
+    assert "bucket invariant violated" not in r.stderr
