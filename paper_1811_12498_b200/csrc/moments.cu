@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "moments.cuh"
+#include "sph_basis.cuh"
 
 namespace st {
 
@@ -42,6 +43,7 @@ constexpr int kTileP = 32;      // particles per shared-memory tile
 constexpr int kChunk = 8192;    // particles per work item
 constexpr int kPmax = 16;
 constexpr int kPow = kPmax + 1; // powers 0..p per axis
+static_assert(kPmax + 2 <= kSphPmax, "solid-harmonic basis table too short");
 
 __device__ __forceinline__ int find_item(const int32_t* __restrict__ off, int n, int item) {
     int lo = 0, hi = n - 1;
@@ -386,17 +388,27 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
     __syncthreads();
+    // Change of basis per grade s, k3 <= 1 Taylor coefficients -> scaled real solid
+    // harmonics (sph_basis.cuh, exact rationals from scripts/gen_sph_basis.py):
+    // W_hat[m] = sum_j B_s[j][m] W[j], so far_eval sums W_hat against harmonics that cost
+    // two DP ops each instead of the 4-5 of the Coulomb recurrence.
     const int H = harm_count(P);
     double* Wb = W + (size_t)blockIdx.x * H * 4;
     for (int h = threadIdx.x; h < H; h += blockDim.x) {
         int s = 0;
         while ((s + 1) * (s + 1) <= h) ++s;
-        const int j = h - s * s;
-        int k1, k2, k3;
-        if (j <= s) { k1 = s - j; k2 = j; k3 = 0; }
-        else { k2 = j - s - 1; k1 = s - 1 - k2; k3 = 1; }
-        const int f = mi_flat(k1, k2, k3);
-        for (int c = 0; c < 4; ++c) Wb[4 * h + c] = s_w[4 * f + c];
+        const int m = h - s * s, n = 2 * s + 1;
+        const double* B = kSphB + sph_off(s);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int j = 0; j < n; ++j) {
+            int k1, k2, k3;
+            if (j <= s) { k1 = s - j; k2 = j; k3 = 0; }
+            else { k2 = j - s - 1; k1 = s - 1 - k2; k3 = 1; }
+            const int f = mi_flat(k1, k2, k3);
+            const double b = B[j * n + m];
+            for (int c = 0; c < 4; ++c) acc[c] = fma(b, s_w[4 * f + c], acc[c]);
+        }
+        for (int c = 0; c < 4; ++c) Wb[4 * h + c] = acc[c];
     }
 }
 

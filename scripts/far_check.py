@@ -27,7 +27,8 @@ if sys.argv[1] == "--compare":
         if k.startswith("u"):
             same = np.array_equal(a[k], b[k])
             ok &= same
-            print(k, "bit-identical" if same else f"DIFFER max {np.max(np.abs(a[k] - b[k])):.3e}",
+            rel = np.linalg.norm(a[k] - b[k]) / np.linalg.norm(a[k])
+            print(k, "bit-identical" if same else f"DIFFER max {np.max(np.abs(a[k] - b[k])):.3e} rel L2 {rel:.2e}",
                   f"far {a['f' + k[1:]][0] * 1e3:.2f} -> {b['f' + k[1:]][0] * 1e3:.2f} ms")
     sys.exit(0 if ok else 1)
 
