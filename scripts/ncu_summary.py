@@ -67,9 +67,14 @@ def launches(path):
 
 def main():
     tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    cfg = os.environ.get("NCU_CFG", "cfg1")  # which BASELINE configuration the captures ran
+    desc = {"cfg1": "cfg1 (N=1M cube, p=8, theta=0.5, N0=2000)",
+            "cfg2": "cfg2 (N=4M sphere, p=10, theta=0.7, N0=2000)",
+            "cfg3": "cfg3 (N=16M cube, p=8, theta=0.5, N0=4000)",
+            "cfg4": "cfg4 (8M Gaussian-mixture sources, 8M uniform targets, p=8, theta=0.6, N0=2000)"}[cfg]
     print(f"# ncu summary — {tag}\n")
     print("Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
-          "(sm_100a), one launch per kernel, BASELINE cfg1 (N=1M cube, p=8, theta=0.5, N0=2000). "
+          f"(sm_100a), one launch per kernel, BASELINE {desc}. "
           "ncu times are cold-cache and serialised: compare shares, not absolutes.\n")
     tot, cnt = launches(lcsv)
     # a bench.py launch list also holds its live FP64 peak probe (not part of a step) and
@@ -93,7 +98,7 @@ def main():
         hdr, units, data = raw(rep)
         for row in data:
             name = row[hdr.index("Kernel Name")] if "Kernel Name" in hdr else rep
-            short = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "").split("(")[0]
+            short = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "").replace("void ", "").split("(")[0]
             print(f"## `{short}` ({os.path.basename(rep)})\n")
             print("| metric | value |\n|---|---|")
             vals = {}
@@ -106,7 +111,8 @@ def main():
             wr = to_bytes(*vals.get("dram__bytes_write.sum", ("0", "byte")))
             kname = ("near" if ("k_near" in name or "k_neval" in name) else "far_deferred" if "k_feval" in name
                      else "far" if "k_far" in name else name)
-            traffic.setdefault("cfg1", {})[f"{kname}_dram_bytes_per_launch"] = rd + wr
+            traffic.setdefault(cfg, {})[f"{kname}_dram_bytes_per_launch"] = rd + wr
+            traffic[cfg][f"{kname}_kernel"] = f"{short} ({tag} capture)"
             print()
     json.dump(traffic, open(traffic_path, "w"), indent=1)
 
