@@ -320,6 +320,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     // K1: tree over the sources, tree-ordered source records
     DevTree tree;
     build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    const MomentsPlan mplan = plan_moments(tree, s);  // host lists now: K2 below never waits on the host
     if (weights_ready) ST_CUDA(cudaStreamWaitEvent(s, weights_ready, 0));
     DevArray<unsigned long long> vflags(6, s);
     vflags.fill_bytes(0xff);
@@ -340,12 +341,19 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     count_launch();
     e1.record(s);
 
-    // K2: moments at order p, folded into the harmonic far-field weights
+    // K2: moments at order p, folded into the far-field weights, on a second stream: only
+    // the far field needs them, so they overlap the target ordering, the plan walks and
+    // the near field (launch_eval waits for `e2` before the far kernels).  Declared before
+    // M and W, whose stream-ordered frees go to it.
+    AuxStream aux;
+    ST_CUDA(cudaStreamWaitEvent(aux.s, e1.e, 0));
+    Event em;
+    em.record(aux.s);
     DevArray<double> M, W;
-    compute_moments_device(tree, rec.get(), prm.order, sto, str, s, M);
-    fold_weights_device(M.get(), tree.ncl, prm.order, sto, str, s, W);
+    compute_moments_device(tree, rec.get(), prm.order, sto, str, aux.s, M, &mplan);
+    fold_weights_device(M.get(), tree.ncl, prm.order, sto, str, aux.s, W);
     M.reset();
-    e2.record(s);
+    e2.record(aux.s);
 
     // batch order of the targets: 63-bit Morton order in their tight box (one radix sort)
     const double* tpos = same ? src.pos : d_targets;
@@ -413,7 +421,8 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     fo.ufar = ufar.get();
     fo.out = d_out;
     EvalTimes tm;
-    launch_eval(sto, str, a, &fo, 1, s, &tm);
+    tm.origin = e0.e;
+    launch_eval(sto, str, a, &fo, 1, s, &tm, e2.e);
     e3.record(s);
 
     ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -421,13 +430,18 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ST_CUDA(cudaMemcpyAsync(ro.vflags, vflags.get(), sizeof ro.vflags, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
     ro.t_build = secs(e0, e1);
-    ro.t_moments = secs(e1, e2);
-    ro.t_traverse = secs(e2, e3);
+    ro.t_moments = secs(em, e2);    // on the second stream, overlapped with the traversal
+    ro.t_traverse = secs(e1, e3);   // targets, plan walks, far and near fields, reduce
     ro.t_total = secs(e0, e3);
     // kernel times: far = dense events (k_far_list) + deferred sparse events (k_feval);
     // near = the leaf sums (k_neval).  Walks, scans and the reduce count in t_traverse only.
     ro.t_far = tm.far_s;
     ro.t_near = tm.near_s;
+    static const bool timeline = getenv("ST_DEBUG_TIMELINE") != nullptr;
+    if (timeline)  // ms from the call's first event: when each phase started / ended
+        fprintf(stderr, "[timeline] build end %.3f | moments %.3f - %.3f (aux stream) | near %.3f - %.3f | "
+                "far start %.3f | end %.3f\n", 1e3 * ro.t_build, 1e3 * secs(e0, em), 1e3 * secs(e0, e2),
+                1e3 * tm.near_start_s, 1e3 * (tm.near_start_s + tm.near_s), 1e3 * tm.far_start_s, 1e3 * ro.t_total);
     if (so) {
         so->w0 = a.w0;
         so->w1 = a.w1;
@@ -482,6 +496,7 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     e0.record(s);
     DevTree tree;
     build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    const MomentsPlan mplan = plan_moments(tree, s);
     DevArray<unsigned long long> vflags(6, s);
     vflags.fill_bytes(0xff);
     k_validate<<<nblocks(n, 256), 256, 0, s>>>(n, src.pos, sto ? src.f : nullptr, str ? src.h : nullptr,
@@ -498,9 +513,14 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     ST_LAUNCH("k_pack");
     count_launch(3);
     e1.record(s);
+    // moments at the largest order and every order's fold on a second stream (see
+    // run_treecode); the far kernels wait for e2
+    AuxStream aux;
+    ST_CUDA(cudaStreamWaitEvent(aux.s, e1.e, 0));
+    Event em;
+    em.record(aux.s);
     DevArray<double> M;
-    compute_moments_device(tree, rec.get(), pmax, sto, str, s, M);
-    e2.record(s);
+    compute_moments_device(tree, rec.get(), pmax, sto, str, aux.s, M, &mplan);
     const double* tpos = same ? src.pos : d_targets;
     DevArray<uint32_t> tperm;
     order_targets(tpos, nt, s, tperm);
@@ -535,15 +555,17 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     std::vector<DevArray<double>> Ws(n_orders), ufars(n_orders);
     std::vector<FarOrder> fo(n_orders);
     for (int i = 0; i < n_orders; ++i) {
-        fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, s, Ws[i], pmax);
+        fold_weights_device(M.get(), tree.ncl, orders[i], sto, str, aux.s, Ws[i], pmax);
         ufars[i].alloc(3 * nt, s);
         fo[i].P = orders[i] + (str ? 2 : 1);
         fo[i].W = Ws[i].get();
         fo[i].ufar = ufars[i].get();
         fo[i].out = d_out + 3 * nt * i;
     }
+    M.reset();
+    e2.record(aux.s);
     EvalTimes tm;
-    launch_eval(sto, str, a, fo.data(), n_orders, s, &tm);
+    launch_eval(sto, str, a, fo.data(), n_orders, s, &tm, e2.e);
     for (int i = 0; i < n_orders; ++i)
         if (far_s) far_s[i] = tm.far_order[i];
     e3.record(s);
@@ -552,8 +574,8 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     ST_CUDA(cudaMemcpyAsync(ro.vflags, vflags.get(), sizeof ro.vflags, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
     ro.t_build = secs(e0, e1);
-    ro.t_moments = secs(e1, e2);
-    ro.t_traverse = secs(e2, e3);
+    ro.t_moments = secs(em, e2);    // on the second stream, overlapped with the traversal
+    ro.t_traverse = secs(e1, e3);   // targets, plan walks, far and near fields, reduce
     ro.t_total = secs(e0, e3);
 }
 

@@ -462,8 +462,37 @@ void launch_moments_ept(bool sto, bool str, dim3 g, int threads, cudaStream_t s,
 
 }  // namespace
 
+MomentsPlan plan_moments(const DevTree& tree, cudaStream_t s) {
+    MomentsPlan pl;
+    const int ncl = tree.ncl;
+    // leaves: direct sums over their particles; internal clusters: M2M by level
+    std::vector<int4> info(ncl);
+    ST_CUDA(cudaMemcpyAsync(info.data(), tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> bylevel(ncl);
+    ST_CUDA(cudaMemcpyAsync(bylevel.data(), tree.bylevel.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaStreamSynchronize(s));
+    for (int v = 0; v < ncl; ++v) {
+        if (!info[v].w) continue;  // internal cluster
+        const int cnt = info[v].y - info[v].x;
+        const int nch = std::max(1, (cnt + kChunk - 1) / kChunk);
+        pl.cl.push_back(v);
+        pl.off.push_back(pl.items);
+        pl.slot.push_back(nch > 1 ? pl.parts : -1);
+        if (nch > 1) pl.parts += nch;
+        pl.items += nch;
+    }
+    pl.off.push_back(pl.items);
+    for (size_t d = 0; d + 1 < tree.level_start.size(); ++d) {
+        std::vector<int32_t> ids;
+        for (int b = tree.level_start[d]; b < tree.level_start[d + 1]; ++b)
+            if (!info[bylevel[b]].w) ids.push_back(bylevel[b]);
+        pl.lv.push_back(ids);
+    }
+    return pl;
+}
+
 void compute_moments_device(const DevTree& tree, const double* src, int p, bool sto, bool str,
-                            cudaStream_t s, DevArray<double>& M) {
+                            cudaStream_t s, DevArray<double>& M, const MomentsPlan* plan) {
     static const bool dbg = getenv("ST_DEBUG_MOMENTS") != nullptr;
     auto stamp = [&](const char* what) {
         if (!dbg) return;
@@ -477,38 +506,19 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
     if (p < 0 || p > kPmax) fail(ST_INVALID_ARGUMENT, "compute_moments: order outside table range");
     const int E = mi_count(p);
     const int ncl = tree.ncl;
-    // leaves: direct sums over their particles; internal clusters: M2M by level (below)
-    std::vector<int4> info(ncl);
-    ST_CUDA(cudaMemcpyAsync(info.data(), tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> bylevel(ncl);
-    ST_CUDA(cudaMemcpyAsync(bylevel.data(), tree.bylevel.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
-    ST_CUDA(cudaStreamSynchronize(s));
-    std::vector<int32_t> off, cl, slot;
-    int items = 0, parts = 0;
-    for (int v = 0; v < ncl; ++v) {
-        if (!info[v].w) continue;  // internal cluster
-        const int cnt = info[v].y - info[v].x;
-        const int nch = std::max(1, (cnt + kChunk - 1) / kChunk);
-        cl.push_back(v);
-        off.push_back(items);
-        slot.push_back(nch > 1 ? parts : -1);
-        if (nch > 1) parts += nch;
-        items += nch;
+    MomentsPlan own;
+    if (!plan) {
+        own = plan_moments(tree, s);
+        plan = &own;
     }
+    const std::vector<int32_t>&off = plan->off, &cl = plan->cl, &slot = plan->slot;
+    const int items = plan->items, parts = plan->parts;
+    const std::vector<std::vector<int32_t>>& lv = plan->lv;
     const int nleaf = (int)cl.size();
-    off.push_back(items);
     DevArray<int32_t> d_off(nleaf + 1, s), d_cl(nleaf, s), d_slot(nleaf, s), d_lvl(ncl, s);
     ST_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), sizeof(int32_t) * (nleaf + 1), cudaMemcpyHostToDevice, s));
     ST_CUDA(cudaMemcpyAsync(d_cl.get(), cl.data(), sizeof(int32_t) * nleaf, cudaMemcpyHostToDevice, s));
     ST_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(int32_t) * nleaf, cudaMemcpyHostToDevice, s));
-    // internal clusters of each level, deepest level last in `lv`
-    std::vector<std::vector<int32_t>> lv;
-    for (size_t d = 0; d + 1 < tree.level_start.size(); ++d) {
-        std::vector<int32_t> ids;
-        for (int b = tree.level_start[d]; b < tree.level_start[d + 1]; ++b)
-            if (!info[bylevel[b]].w) ids.push_back(bylevel[b]);
-        lv.push_back(ids);
-    }
     {
         std::vector<int32_t> flat;
         for (const auto& ids : lv) flat.insert(flat.end(), ids.begin(), ids.end());

@@ -2,16 +2,29 @@
 // far-field weights the traversal kernels contract with.
 #pragma once
 
+#include <vector>
+
 #include "st_common.cuh"
 #include "tree.cuh"
 
 namespace st {
 
+// Host-side work lists of the moment pass (leaf items and chunk partials, internal
+// clusters by level), built from the tree's cluster records read back on stream `s`
+// (one synchronisation).  Independent of the order p.
+struct MomentsPlan {
+    std::vector<int32_t> off, cl, slot;  // leaf work items: first item, cluster, partial slot
+    int items = 0, parts = 0;
+    std::vector<std::vector<int32_t>> lv;  // internal clusters per level, root level first
+};
+MomentsPlan plan_moments(const DevTree& tree, cudaStream_t s);
+
 // Cartesian moments of every cluster at order p, combined layout
 // M[ncl][E(p)][12]: columns 0..2 = M_j^k (f), 3..11 = M~_jl^k (h_j nu_l, j*3+l).
-// `src` is the tree-ordered 12-double source record array.
+// `src` is the tree-ordered 12-double source record array.  With a plan, nothing in
+// here waits for the host: the kernels can be queued on a second stream.
 void compute_moments_device(const DevTree& tree, const double* src, int p, bool sto, bool str,
-                            cudaStream_t s, DevArray<double>& M);
+                            cudaStream_t s, DevArray<double>& M, const MomentsPlan* plan = nullptr);
 
 // Far-field weights in the harmonic basis: W[ncl][(P+1)^2][4] with
 // u_i = sum_h b_h W[h][i] + dx_i * sum_h b_h W[h][3]  ("K4").

@@ -49,6 +49,16 @@ struct Event {
     }
     void record(cudaStream_t s) { ST_CUDA(cudaEventRecord(e, s)); }
 };
+// A non-blocking stream owned by one call (destroyed after its queued work completes).
+struct AuxStream {
+    cudaStream_t s = nullptr;
+    AuxStream() { ST_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    AuxStream(const AuxStream&) = delete;
+    AuxStream& operator=(const AuxStream&) = delete;
+    ~AuxStream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
 inline double secs(const Event& a, const Event& b) {
     float ms = 0.f;
     ST_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));

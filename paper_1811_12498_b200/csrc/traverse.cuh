@@ -44,14 +44,18 @@ struct EvalTimes {
     double near_s = 0.0;            // k_neval (all slabs)
     double far_s = 0.0;             // k_far_list + k_feval (all slabs and orders)
     std::vector<double> far_order;  // the same per order
+    cudaEvent_t origin = nullptr;   // if set: start of the first near / far launch after it
+    double near_start_s = 0.0, far_start_s = 0.0;
 };
 // K3-K5 for the batch warps [a.w0, a.w1): the plan walks (counts, then near entries,
 // deferred sparse far entries and each warp's dense far events), then per slab the dense
 // far field of every order, the near field once, the packed sparse far events and the
 // reduce per order (original order unless a.out_batch); counters into a.stats and
 // a.per_target.  Synchronises the stream before returning.
+// far_ready (if set): the orders' weights W are produced on another stream; the far
+// kernels wait for it (they run after the near field's evaluation).
 void launch_eval(bool sto, bool str, const TravArgs& a, const FarOrder* orders, int n_orders, cudaStream_t s,
-                 EvalTimes* times = nullptr);
+                 EvalTimes* times = nullptr, cudaEvent_t far_ready = nullptr);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
