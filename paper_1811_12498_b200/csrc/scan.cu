@@ -1,5 +1,8 @@
 #include "scan.cuh"
 
+#include <cub/device/device_scan.cuh>
+#include <thrust/iterator/transform_iterator.h>
+
 namespace st {
 
 namespace {
@@ -94,10 +97,31 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_u32_u64(const uint32_t* _
     if (threadIdx.x == 0) out[nrows] = carry;
 }
 
+namespace {
+struct ToU64 {
+    __host__ __device__ uint64_t operator()(uint32_t v) const { return v; }
+};
+// Rows beyond one CTA's comfortable range go to CUB's decoupled-lookback scan (single-CTA
+// scans of 250K rows took 0.26 ms each at cfg4); small ones stay one launch.
+constexpr int kScanOneCta = 16384;
+}  // namespace
+
 void launch_scan_u32_u64(const uint32_t* in, uint64_t* out, int nrows, cudaStream_t s) {
-    k_scan_u32_u64<<<1, kScanThreads, 0, s>>>(in, out, nrows);
-    ST_LAUNCH("k_scan_u32_u64");
-    count_launch();
+    if (nrows <= kScanOneCta) {
+        k_scan_u32_u64<<<1, kScanThreads, 0, s>>>(in, out, nrows);
+        ST_LAUNCH("k_scan_u32_u64");
+        count_launch();
+        return;
+    }
+    // out[0] = 0, out[1..n] = inclusive sums (accumulated in 64 bits)
+    const auto it = thrust::make_transform_iterator(in, ToU64());
+    size_t tmp = 0;
+    ST_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, it, out + 1, nrows, s));
+    DevArray<unsigned char> scratch(tmp, s);
+    ST_CUDA(cudaMemsetAsync(out, 0, sizeof(uint64_t), s));
+    ST_CUDA(cub::DeviceScan::InclusiveSum(scratch.get(), tmp, it, out + 1, nrows, s));
+    ST_LAUNCH("cub::DeviceScan (u32 -> u64)");
+    count_launch(2);
 }
 
 void launch_scan_cols(const uint32_t* in, uint32_t* out, int nrows, int ncols, cudaStream_t s) {
@@ -107,9 +131,19 @@ void launch_scan_cols(const uint32_t* in, uint32_t* out, int nrows, int ncols, c
 }
 
 void launch_scan_i32(const int32_t* in, int32_t* out, int nrows, cudaStream_t s) {
-    k_scan_i32<<<1, kScanThreads, 0, s>>>(in, out, nrows);
-    ST_LAUNCH("k_scan_i32");
-    count_launch();
+    if (nrows <= kScanOneCta) {
+        k_scan_i32<<<1, kScanThreads, 0, s>>>(in, out, nrows);
+        ST_LAUNCH("k_scan_i32");
+        count_launch();
+        return;
+    }
+    size_t tmp = 0;
+    ST_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out + 1, nrows, s));
+    DevArray<unsigned char> scratch(tmp, s);
+    ST_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), s));
+    ST_CUDA(cub::DeviceScan::InclusiveSum(scratch.get(), tmp, in, out + 1, nrows, s));
+    ST_LAUNCH("cub::DeviceScan (i32)");
+    count_launch(2);
 }
 
 }  // namespace st
