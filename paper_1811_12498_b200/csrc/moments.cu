@@ -33,13 +33,17 @@
 
 #include "moments.cuh"
 #include "sph_basis.cuh"
+#include "tma.cuh"
 
 namespace st {
 
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kTileP = 32;      // particles per shared-memory tile
+#ifndef ST_MOMENTS_TILE
+#define ST_MOMENTS_TILE 32
+#endif
+constexpr int kTileP = ST_MOMENTS_TILE;  // particles per shared-memory tile
 constexpr int kChunk = 8192;    // particles per work item
 constexpr int kPmax = 16;
 constexpr int kPow = kPmax + 1; // powers 0..p per axis
@@ -108,28 +112,40 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int c = 0; c < NCP; ++c) acc[j][c] = 0.0;
 
-    for (int t0 = b; t0 < e_end; t0 += kTileP) {
+    // the tile's contiguous tree-ordered records arrive by TMA, one tile ahead of the
+    // staging that reads them (no global-load latency between the tiles)
+    __shared__ __align__(128) double s_raw[2][kTileP * 12];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        mbar_fence_init();
+        if (b < e_end) bulk_g2s(s_raw[0], src + 12 * (size_t)b, 96u * min(kTileP, e_end - b), &s_bar[0]);
+    }
+    int it = 0;
+    for (int t0 = b; t0 < e_end; t0 += kTileP, ++it) {
         const int nt = min(kTileP, e_end - t0);
-        __syncthreads();
-        if (threadIdx.x < nt) {
-            const double* r = src + 12 * (size_t)(t0 + threadIdx.x);
-            const double d[3] = {r[0] - g.x, r[1] - g.y, r[2] - g.z};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                double pw = 1.0;
-                s_pow[threadIdx.x][a * kPow] = 1.0;
-                for (int q = 1; q <= p; ++q) {
-                    pw *= d[a];
-                    s_pow[threadIdx.x][a * kPow + q] = pw;
-                }
+        const int cur = it & 1;
+        __syncthreads();  // the previous tile's compute is done with s_pow / s_w
+        if (threadIdx.x == 0 && t0 + kTileP < e_end)  // s_raw[cur ^ 1] was staged last iteration
+            bulk_g2s(s_raw[cur ^ 1], src + 12 * (size_t)(t0 + kTileP), 96u * min(kTileP, e_end - t0 - kTileP),
+                     &s_bar[cur ^ 1]);
+        mbar_wait(&s_bar[cur], (it >> 1) & 1);
+        // one thread per (particle, axis): the axis' power chain, f_a and the row h_a nu_l
+        for (int x = threadIdx.x; x < 3 * nt; x += T) {
+            const int q = x / 3, a = x - 3 * q;
+            const double* r = s_raw[cur] + 12 * q;
+            const double d = r[a] - (a == 0 ? g.x : a == 1 ? g.y : g.z);
+            double pw = 1.0;
+            s_pow[q][a * kPow] = 1.0;
+            for (int k = 1; k <= p; ++k) {
+                pw *= d;
+                s_pow[q][a * kPow + k] = pw;
             }
-            if (STO)
-                for (int c = 0; c < 3; ++c) s_w[threadIdx.x][c] = r[3 + c];
+            if (STO) s_w[q][a] = r[3 + a];
             if (STR)
-                for (int j = 0; j < 3; ++j)
-                    for (int l = 0; l < 3; ++l)
-                        s_w[threadIdx.x][(STO ? 3 : 0) + 3 * j + l] = r[6 + j] * r[9 + l];
-            if (NCP > NC) s_w[threadIdx.x][NCP - 1] = 0.0;
+                for (int l = 0; l < 3; ++l) s_w[q][(STO ? 3 : 0) + 3 * a + l] = r[6 + a] * r[9 + l];
+            if (NCP > NC && a == 0) s_w[q][NCP - 1] = 0.0;
         }
         __syncthreads();
         int kk[EPT][3];
@@ -530,8 +546,12 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
     M.zero();
     DevArray<double> part((size_t)std::max(parts, 1) * E * 12, s);
     stamp("alloc");
-    // entries per thread: 4 amortises the weight loads; block = E/EPT rounded up to a warp
-    const int ept = E >= 128 ? 4 : E >= 32 ? 2 : 1;
+    // entries per thread (block = E/EPT rounded up to a warp): 2 (106 registers) measured
+    // fastest (4: 163 registers, 20% slower at cfg1); 4 once E/2 exceeds the 256-thread
+    // launch bound (p >= 13).  ST_MOMENTS_EPT overrides (A/B checks).
+    static const int ept_env = getenv("ST_MOMENTS_EPT") ? atoi(getenv("ST_MOMENTS_EPT")) : 0;
+    int ept = ept_env == 1 || ept_env == 2 || ept_env == 4 ? ept_env : E >= 32 ? 2 : 1;
+    while ((E + ept - 1) / ept > kThreads) ept *= 2;
     const int threads = std::max(32, ((E + ept - 1) / ept + 31) / 32 * 32);
     if (items) {
         dim3 g(items);
