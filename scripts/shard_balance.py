@@ -23,15 +23,31 @@ prm = S.TreecodeParams(order=cfg["order"], theta=cfg["theta"], leaf_capacity=cfg
 b, st = dsrc.data_ptr(), n * 24
 stream = torch.cuda.current_stream().cuda_stream
 for rep in range(2):
-    times = []
+    times, calls = [], []
     for r in range(k):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         res = S.treecode_velocity_device(b, b + st, b + 2 * st, b + 3 * st, n, prm, dout.data_ptr(),
                                          targets_ptr=None if dtg is None else dtg.data_ptr(),
                                          n_targets=nt if dtg is not None else 0, shard=r, n_shards=k, stream=stream)
+        e1.record()
+        torch.cuda.synchronize()
         times.append(1e3 * (res.time_far_s + res.time_near_s))
+        calls.append(e0.elapsed_time(e1))  # the whole shard call: what one rank's step costs
 full = S.treecode_velocity_device(b, b + st, b + 2 * st, b + 3 * st, n, prm, dout.data_ptr(),
                                   targets_ptr=None if dtg is None else dtg.data_ptr(),
                                   n_targets=nt if dtg is not None else 0, stream=stream)
 ideal = 1e3 * (full.time_far_s + full.time_near_s) / k
 print(sys.argv[1], k, "shards far+near ms:", [round(x, 2) for x in times], "max/ideal",
       round(max(times) / ideal, 3), "total/k", round(sum(times) / k, 2), "ideal", round(ideal, 2))
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+S.treecode_velocity_device(b, b + st, b + 2 * st, b + 3 * st, n, prm, dout.data_ptr(),
+                           targets_ptr=None if dtg is None else dtg.data_ptr(),
+                           n_targets=nt if dtg is not None else 0, stream=stream)
+e1.record()
+torch.cuda.synchronize()
+one = e0.elapsed_time(e1)
+print(sys.argv[1], k, "whole shard calls ms:", [round(x, 2) for x in calls], "one GPU", round(one, 2),
+      "-> projected step", round(max(calls), 2), "efficiency", round(one / (k * max(calls)), 3),
+      "(no NVLink stores / all-reduce; shards run one at a time)")
