@@ -316,6 +316,16 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     if (nt >= 0x7fffffffull - 64) fail(ST_INVALID_ARGUMENT, "too many targets");
     Event e0, e1, e2, e3;
     e0.record(s);
+    // Second stream: the targets' Morton order (positions only) overlaps the tree build's
+    // host-synchronised levels; then K2 (below).  Declared before every array whose
+    // stream-ordered free goes to it.
+    AuxStream aux;
+    ST_CUDA(cudaStreamWaitEvent(aux.s, e0.e, 0));
+    const double* tpos = same ? src.pos : d_targets;
+    DevArray<uint32_t> tperm;
+    order_targets(tpos, nt, aux.s, tperm);
+    Event esort;
+    esort.record(aux.s);
 
     // K1: tree over the sources, tree-ordered source records
     DevTree tree;
@@ -341,11 +351,9 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     count_launch();
     e1.record(s);
 
-    // K2: moments at order p, folded into the far-field weights, on a second stream: only
-    // the far field needs them, so they overlap the target ordering, the plan walks and
-    // the near field (launch_eval waits for `e2` before the far kernels).  Declared before
-    // M and W, whose stream-ordered frees go to it.
-    AuxStream aux;
+    // K2: moments at order p, folded into the far-field weights, on the second stream: only
+    // the far field needs them, so they overlap the plan walks and the near field
+    // (launch_eval waits for `e2` before the far kernels).
     ST_CUDA(cudaStreamWaitEvent(aux.s, e1.e, 0));
     Event em;
     em.record(aux.s);
@@ -355,16 +363,17 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     M.reset();
     e2.record(aux.s);
 
-    // batch order of the targets: 63-bit Morton order in their tight box (one radix sort)
-    const double* tpos = same ? src.pos : d_targets;
-    DevArray<uint32_t> tperm;
-    order_targets(tpos, nt, s, tperm);
+    // batch order of the targets: 63-bit Morton order in their tight box (one radix sort,
+    // done on the second stream above)
+    ST_CUDA(cudaStreamWaitEvent(s, esort.e, 0));
     DevArray<double> tx(3 * nt, s), ufar(3 * nt, s);
     DevArray<uint32_t> torig(nt, s), tskip(nt, s);
     k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr,
                                                tx.get(), torig.get(), tskip.get());
     ST_LAUNCH("k_targets");
     count_launch();
+    Event et, ec;  // timeline: targets ordered, shard cuts known
+    et.record(s);
 
     DevArray<unsigned long long> d_stats(3, s);
     DevArray<int> d_err(1, s), d_work(2, s);
@@ -404,8 +413,9 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         std::vector<float> hc(nwarps);
         ST_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), sizeof(float) * nwarps, cudaMemcpyDeviceToHost, s));
         ST_CUDA(cudaStreamSynchronize(s));
-        for (int w = 0; w < nwarps; ++w)  // every kCountStride-th warp was sampled
-            if (w % kCountStride) hc[w] = hc[w - w % kCountStride];
+        const int stride = count_stride(nwarps);
+        for (int w = 0; w < nwarps; ++w)  // every stride-th warp was sampled
+            if (w % stride) hc[w] = hc[w - w % stride];
         std::vector<double> w(hc.begin(), hc.end());
         std::vector<size_t> cuts(nshards + 1);
         shard_cuts_host(nwarps, w.data(), nshards, cuts.data());
@@ -413,6 +423,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         a.w1 = (int)cuts[shard + 1];
         a.warp_cost = nullptr;
     }
+    ec.record(s);
 
     a.sparse_max = far_sparse_max();
     FarOrder fo;
@@ -439,9 +450,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ro.t_near = tm.near_s;
     static const bool timeline = getenv("ST_DEBUG_TIMELINE") != nullptr;
     if (timeline)  // ms from the call's first event: when each phase started / ended
-        fprintf(stderr, "[timeline] build end %.3f | moments %.3f - %.3f (aux stream) | near %.3f - %.3f | "
-                "far start %.3f | end %.3f\n", 1e3 * ro.t_build, 1e3 * secs(e0, em), 1e3 * secs(e0, e2),
-                1e3 * tm.near_start_s, 1e3 * (tm.near_start_s + tm.near_s), 1e3 * tm.far_start_s, 1e3 * ro.t_total);
+        fprintf(stderr, "[timeline] build end %.3f | moments %.3f - %.3f (aux stream) | targets ordered %.3f | "
+                "cuts %.3f | near %.3f - %.3f | far start %.3f | end %.3f\n", 1e3 * ro.t_build, 1e3 * secs(e0, em),
+                1e3 * secs(e0, e2), 1e3 * secs(e0, et), 1e3 * secs(e0, ec), 1e3 * tm.near_start_s,
+                1e3 * (tm.near_start_s + tm.near_s), 1e3 * tm.far_start_s, 1e3 * ro.t_total);
     if (so) {
         so->w0 = a.w0;
         so->w1 = a.w1;

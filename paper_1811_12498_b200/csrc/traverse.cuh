@@ -62,6 +62,9 @@ void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64
 // Traversal-only work estimate of every 4th warp of [a.w0, a.w1) into a.warp_cost (for
 // multi-GPU shard cuts; the caller fills the warps in between from the preceding sample).
 constexpr int kCountStride = 4;
+// every count_stride(w)-th of w batch warps is walked for the shard cuts: at least every
+// 4th, at most ~8K samples (the per-warp cost is smooth along the Morton order)
+inline int count_stride(int warps) { return warps / 8192 > kCountStride ? warps / 8192 : kCountStride; }
 void launch_count(const TravArgs& a, float far_cost, float near_cost, cudaStream_t s);
 
 // O(N^2) contracted direct sum (kernels.hpp:45-83, 123-150): sources are the
