@@ -132,6 +132,25 @@ __global__ void k_pack(size_t n, const uint32_t* __restrict__ perm, const double
     if (to_tree) to_tree[o] = (uint32_t)t;
 }
 
+// The same records written from the original order: coalesced reads of the caller's
+// arrays, each record stored whole (six 16-byte stores) at its tree position.
+__global__ void k_pack_tree(size_t n, const uint32_t* __restrict__ to_tree, const double* __restrict__ pos,
+                            const double* __restrict__ f, const double* __restrict__ h,
+                            const double* __restrict__ nu, double* __restrict__ rec) {
+    const size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    double v[12];
+    for (int a = 0; a < 3; ++a) {
+        v[a] = pos[3 * o + a];
+        v[3 + a] = f ? f[3 * o + a] : 0.0;
+        v[6 + a] = h ? h[3 * o + a] : 0.0;
+        v[9 + a] = nu ? nu[3 * o + a] : 0.0;
+    }
+    double2* r = reinterpret_cast<double2*>(rec + 12 * (size_t)to_tree[o]);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) r[q] = make_double2(v[2 * q], v[2 * q + 1]);
+}
+
 // Targets in batch order: positions, original index, excluded source tree index.
 __global__ void k_targets(size_t nt, const uint32_t* __restrict__ tperm, const double* __restrict__ tpos,
                           const uint32_t* __restrict__ to_tree, double* __restrict__ tx,
@@ -343,11 +362,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     }
     count_launch(d_targets ? 2 : 1);
     DevArray<double> rec(12 * n, s);
-    DevArray<uint32_t> to_tree(n, s);
-    k_pack<<<nblocks(n, 256), 256, 0, s>>>(n, tree.perm.get(), src.pos, sto ? src.f : nullptr,
-                                           str ? src.h : nullptr, str ? src.nu : nullptr, rec.get(),
-                                           to_tree.get());
-    ST_LAUNCH("k_pack");
+    const DevArray<uint32_t>& to_tree = tree.to_tree;
+    k_pack_tree<<<nblocks(n, 256), 256, 0, s>>>(n, to_tree.get(), src.pos, sto ? src.f : nullptr,
+                                                str ? src.h : nullptr, str ? src.nu : nullptr, rec.get());
+    ST_LAUNCH("k_pack_tree");
     count_launch();
     e1.record(s);
 
@@ -519,10 +537,10 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
         ST_LAUNCH("k_validate");
     }
     DevArray<double> rec(12 * n, s);
-    DevArray<uint32_t> to_tree(n, s);
-    k_pack<<<nblocks(n, 256), 256, 0, s>>>(n, tree.perm.get(), src.pos, sto ? src.f : nullptr,
-                                           str ? src.h : nullptr, str ? src.nu : nullptr, rec.get(), to_tree.get());
-    ST_LAUNCH("k_pack");
+    const DevArray<uint32_t>& to_tree = tree.to_tree;
+    k_pack_tree<<<nblocks(n, 256), 256, 0, s>>>(n, to_tree.get(), src.pos, sto ? src.f : nullptr,
+                                                str ? src.h : nullptr, str ? src.nu : nullptr, rec.get());
+    ST_LAUNCH("k_pack_tree");
     count_launch(3);
     e1.record(s);
     // moments at the largest order and every order's fold on a second stream (see

@@ -389,11 +389,11 @@ __device__ __forceinline__ int find_item(const int32_t* __restrict__ off, int T,
 }
 
 // Shrink: tight box of each cluster's range (cluster_tree.hpp:88), exact min/max.
+// `tpos`: positions in tree order (k_tree_pos), read contiguously per cluster range.
 __global__ void __launch_bounds__(256) k_minmax(int T, const int32_t* __restrict__ item_off,
                                                 const uint32_t* __restrict__ nb_begin,
                                                 const uint32_t* __restrict__ nb_end,
-                                                const uint32_t* __restrict__ perm,
-                                                const double* __restrict__ pos,
+                                                const double* __restrict__ tpos,
                                                 unsigned long long* __restrict__ mm) {
     const int item = blockIdx.x;
     const int v = find_item(item_off, T, item);
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(256) k_minmax(int T, const int32_t* __restrict
     const uint32_t e = min(nb_end[v], b + kGeomChunk);
     uint64_t lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
     for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-        const double* p = pos + 3 * (size_t)perm[t];
+        const double* p = tpos + 3 * (size_t)t;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const uint64_t q = ord_enc(p[a]);
@@ -443,8 +443,7 @@ __global__ void k_center(int T, int shrink, const unsigned long long* __restrict
 __global__ void __launch_bounds__(256) k_radius(int T, const int32_t* __restrict__ item_off,
                                                 const uint32_t* __restrict__ nb_begin,
                                                 const uint32_t* __restrict__ nb_end,
-                                                const uint32_t* __restrict__ perm,
-                                                const double* __restrict__ pos,
+                                                const double* __restrict__ tpos,
                                                 const double* __restrict__ center,
                                                 unsigned long long* __restrict__ r2max) {
     const int item = blockIdx.x;
@@ -454,13 +453,31 @@ __global__ void __launch_bounds__(256) k_radius(int T, const int32_t* __restrict
     const double c0 = center[3 * v], c1 = center[3 * v + 1], c2 = center[3 * v + 2];
     uint64_t m = 0;
     for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-        const double* p = pos + 3 * (size_t)perm[t];
+        const double* p = tpos + 3 * (size_t)t;
         const double r2 = norm2_rn(__dsub_rn(p[0], c0), __dsub_rn(p[1], c1), __dsub_rn(p[2], c2));
         const uint64_t q = static_cast<uint64_t>(__double_as_longlong(r2));
         m = m < q ? q : m;
     }
     m = warp_max(m);
     if ((threadIdx.x & 31) == 0) atomicMax(&r2max[v], (unsigned long long)m);
+}
+
+// to_tree[perm[t]] = t
+__global__ void k_invperm(uint32_t n, const uint32_t* __restrict__ perm, uint32_t* __restrict__ to_tree) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) to_tree[perm[t]] = t;
+}
+
+// positions in tree order, once, so the geometry passes over every level read them
+// contiguously (they gathered 24-byte records through perm per level before)
+__global__ void k_tree_pos(uint32_t n, const uint32_t* __restrict__ perm, const double* __restrict__ pos,
+                           double* __restrict__ tpos) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double* p = pos + 3 * (size_t)perm[t];
+    tpos[3 * (size_t)t] = p[0];
+    tpos[3 * (size_t)t + 1] = p[1];
+    tpos[3 * (size_t)t + 2] = p[2];
 }
 
 __global__ void k_finalize(int T, int geometry, const int32_t* __restrict__ pre,
@@ -664,6 +681,10 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         launch_scan_i32(nck.get(), ioff.get(), T, s);
         count_launch();
         const int items = read_i32(ioff.get() + T, s);
+        DevArray<double> tpos(3 * (size_t)n, s);
+        k_tree_pos<<<blocks(n, 256), 256, 0, s>>>(n, perm.get(), d_pos, tpos.get());
+        ST_LAUNCH("k_tree_pos");
+        count_launch();
         center.alloc(3 * (size_t)T, s);
         fbox.alloc(6 * (size_t)T, s);
         r2max.alloc(T, s);
@@ -675,16 +696,15 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
             nmm.fill_bytes(0xff);
             k_zero_hi<<<blocks(T, 256), 256, 0, s>>>(nmm.get(), T);
             ST_LAUNCH("k_zero_hi");
-            k_minmax<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), perm.get(), d_pos,
-                                           nmm.get());
+            k_minmax<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), tpos.get(), nmm.get());
             ST_LAUNCH("k_minmax");
             count_launch(2);
         }
         k_center<<<blocks(T, 128), 128, 0, s>>>(T, shrink ? 1 : 0, nmm.get(), nb_box.get(), fbox.get(),
                                                 center.get());
         ST_LAUNCH("k_center");
-        k_radius<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), perm.get(), d_pos,
-                                       center.get(), r2max.get());
+        k_radius<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), tpos.get(), center.get(),
+                                       r2max.get());
         ST_LAUNCH("k_radius");
         count_launch(2);
     }
@@ -694,6 +714,10 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
                                               out.bbox.get(), out.children.get(), out.nchild.get(),
                                               out.bylevel.get());
     ST_LAUNCH("k_finalize");
+    count_launch();
+    out.to_tree.alloc(n, s);
+    k_invperm<<<blocks(n, 256), 256, 0, s>>>(n, perm.get(), out.to_tree.get());
+    ST_LAUNCH("k_invperm");
     count_launch();
     out.perm = std::move(perm);
 }

@@ -18,6 +18,7 @@ struct DevTree {
     DevArray<int32_t> children;  // 8 per cluster, pre-order ids, -1 padded
     DevArray<int32_t> nchild;    // n_children
     DevArray<uint32_t> perm;     // tree index -> original index (to_original)
+    DevArray<uint32_t> to_tree;  // original index -> tree index (the inverse of perm)
     DevArray<int32_t> bylevel;   // pre-order ids in breadth-first (level) order
     std::vector<int> level_start;  // host: bylevel[level_start[d] .. level_start[d+1]) = depth d
 };
