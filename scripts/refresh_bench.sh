@@ -11,3 +11,6 @@ ST_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --n
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${tag}_bench_cfg1.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 for f in gpurun_out/bench_${tag}_*.json; do echo "$f: $(head -c 300 $f)"; done
 tail -2 gpurun_out/bench_${tag}_n2_gloo.log
+# full ncu captures of the two evaluation kernels at cfg1 (current build)
+ncu --set full --clock-control none --import-source on -k regex:k_neval -c 1 -o gpurun_out/neval_${tag} python scripts/profile_step.py cfg1 1 > gpurun_out/ncu_neval.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_far_list -c 1 -o gpurun_out/farlist_${tag} python scripts/profile_step.py cfg1 1 > gpurun_out/ncu_farlist.log 2>&1
