@@ -590,3 +590,27 @@ def test_near_plan_invariants_debug_checker():
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("ok: slabs bit-identical") == 3
     assert "bucket invariant violated" not in r.stderr
+
+
+@pytest.mark.parametrize("ept", ["1", "4"])
+def test_moment_kernel_shapes_bit_identical(S, tmp_path, ept):
+    # the moment kernel's multi-indices per thread (ST_MOMENTS_EPT; default 2) change only
+    # which thread owns a multi-index, not the particle order of its sums: identical bits
+    import os
+    import subprocess
+    import sys
+    ps = S.generate("unit", 30000, 23, True)
+    T = S.build_tree(ps, 700, True)
+    m = S.compute_moments(T, 6, S.KernelSelection.both())
+    out = tmp_path / "m.npz"
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1811_12498_b200 as S; "
+            "ps = S.generate('unit', 30000, 23, True); T = S.build_tree(ps, 700, True); "
+            "m = S.compute_moments(T, 6, S.KernelSelection.both()); "
+            "np.savez(%r, a=m.stok, b=m.str, c=m.trace, d=m.sym)" % (os.path.dirname(os.path.dirname(
+                os.path.abspath(__file__))), str(out)))
+    env = dict(os.environ, ST_MOMENTS_EPT=ept)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    g = np.load(out)
+    for mine, other in ((m.stok, g["a"]), (m.str, g["b"]), (m.trace, g["c"]), (m.sym, g["d"])):
+        assert mine.tobytes() == other.tobytes()
