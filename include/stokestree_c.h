@@ -122,6 +122,15 @@ st_status st_treecode_velocity_device(const st_particles* src_device, const doub
                                       size_t n_targets, const st_params* params,
                                       double* u_out_device, int shard, int n_shards,
                                       void* stream, st_stats* stats);
+/* As st_treecode_velocity_device while the weight arrays (force_weight, dipole_weight,
+ * normal) may still be in flight: the call waits for `weights_ready` (a cudaEvent_t, may
+ * be NULL) after the tree build, which reads positions only -- so a caller uploading its
+ * inputs copies positions (and targets) first and overlaps the rest with the build
+ * (what st_treecode_velocity_ex does internally for host arrays). */
+st_status st_treecode_velocity_device_ev(const st_particles* src_device, const double* targets_device,
+                                         size_t n_targets, const st_params* params,
+                                         double* u_out_device, int shard, int n_shards,
+                                         void* stream, void* weights_ready, st_stats* stats);
 
 /* Order sweep (new): velocities at every order in orders[n_orders] (params->order
  * ignored) from one tree, one moment pass at max(orders) -- order-p moments are the

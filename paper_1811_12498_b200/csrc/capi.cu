@@ -947,6 +947,13 @@ st_status st_ipc_close(void* dptr) {
 st_status st_treecode_velocity_device(const st_particles* src, const double* targets, size_t n_targets,
                                       const st_params* params, double* u_out, int shard, int n_shards,
                                       void* stream, st_stats* stats) {
+    return st_treecode_velocity_device_ev(src, targets, n_targets, params, u_out, shard, n_shards, stream, nullptr,
+                                          stats);
+}
+
+st_status st_treecode_velocity_device_ev(const st_particles* src, const double* targets, size_t n_targets,
+                                         const st_params* params, double* u_out, int shard, int n_shards,
+                                         void* stream, void* weights_ready, st_stats* stats) {
     return guarded([&] {
         g_launches = 0;
         validate_params(params);
@@ -963,7 +970,8 @@ st_status st_treecode_velocity_device(const st_particles* src, const double* tar
         d.h = str ? src->dipole_weight : nullptr;
         d.nu = str ? src->normal : nullptr;
         RunOut ro;
-        run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro);
+        run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro,
+                     false, nullptr, static_cast<cudaEvent_t>(weights_ready));
         raise_flags(ro);
         fill_stats(stats, ro);
         if (stats) stats->gpu_launches = g_launches;

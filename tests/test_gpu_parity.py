@@ -614,3 +614,32 @@ def test_moment_kernel_shapes_bit_identical(S, tmp_path, ept):
     g = np.load(out)
     for mine, other in ((m.stok, g["a"]), (m.str, g["b"]), (m.trace, g["c"]), (m.sym, g["d"])):
         assert mine.tobytes() == other.tobytes()
+
+
+def test_device_call_with_weights_in_flight(S):
+    # st_treecode_velocity_device_ev: the weight arrays arrive on another stream, the call
+    # waits for their event after the tree build; the result equals the plain device call
+    torch = pytest.importorskip("torch")
+    ps = S.generate("cube", 60000, 29, True)
+    n = ps.size()
+    host = torch.from_numpy(np.concatenate([ps.position, ps.force_weight, ps.dipole_weight, ps.normal])).pin_memory()
+    prm = S.TreecodeParams(order=6, theta=0.5, leaf_capacity=500)
+    main = torch.cuda.current_stream()
+    ref = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+    dsrc = host.cuda()
+    b, st = dsrc.data_ptr(), n * 24
+    S.treecode_velocity_device(b, b + st, b + 2 * st, b + 3 * st, n, prm, ref.data_ptr(), stream=main.cuda_stream)
+    dsrc2 = torch.empty_like(dsrc)
+    out = torch.zeros_like(ref)
+    side = torch.cuda.Stream()
+    ready = torch.cuda.Event()
+    dsrc2[:n].copy_(host[:n], non_blocking=True)
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(2_000_000)  # the weights arrive late
+        dsrc2[n:].copy_(host[n:], non_blocking=True)
+        ready.record(side)
+    b2 = dsrc2.data_ptr()
+    S.treecode_velocity_device(b2, b2 + st, b2 + 2 * st, b2 + 3 * st, n, prm, out.data_ptr(),
+                               stream=main.cuda_stream, weights_event=ready.cuda_event)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
