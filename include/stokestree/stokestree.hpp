@@ -474,6 +474,8 @@ inline Vec3 stokeslet_farfield(const Vec3& dx, const StokesletMomentsView& m, in
     abi::check(st_farfield_pairs(1, dx.c, p, 1, 0, m.m.data(), nullptr, nullptr, nullptr, u.c));
     return u;
 }
+// m.trace and m.sym must be the contractions of m.mt (as compute_moments produces them,
+// moments.hpp:66-80): the device path recomputes them from m.mt (stokestree_c.h).
 inline Vec3 stresslet_farfield(const Vec3& dx, const StressletMomentsView& m, int p, const MultiIndexTable& table,
                                const FarFieldWorkspace&) {
     if (table.pmax() < p + 2) throw std::invalid_argument("stresslet_farfield: table too shallow for order");

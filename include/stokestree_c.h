@@ -90,6 +90,13 @@ const char* st_last_error(void);
 /* Number of visible CUDA devices (0 when none / no driver). */
 st_status st_device_count(int* out);
 
+/* Device memory the library keeps between calls on the CURRENT device -- its private
+ * stream-ordered pool (the process's default pool is never reconfigured) and the
+ * near-field entry workspace -- goes back to the driver.  No reference counterpart (the
+ * reference holds no device memory); call it when the host application needs the memory
+ * back.  Synchronises the device. */
+st_status st_release_workspace(void);
+
 /* ---- validation (pure host, no GPU needed) ---- */
 /* TreecodeParams::validate (engine.hpp:31-41). */
 st_status st_params_validate(const st_params* params);
@@ -221,7 +228,11 @@ st_status st_coulomb_coeffs(size_t n_pairs, const double* dx, int pmax, double* 
 st_status st_taylor_coeffs(size_t n_pairs, const double* dx, const double* b, int pmax_b, int order,
                            double* a_sto, double* a_str);
 /* stokeslet_farfield + stresslet_farfield for n_pairs (dx, moment block) pairs; moment
- * blocks in the reference layout, one block of E(p) entries per pair. */
+ * blocks in the reference layout, one block of E(p) entries per pair.  trace and sym
+ * (StressletMomentsView, moments.hpp:103-134) are accepted for the signature but not
+ * read: they are recomputed from str, which is how compute_moments defines them
+ * (derive_stresslet_contractions, moments.hpp:66-80).  A caller whose trace/sym are not the contractions of its str
+ * gets the far field of str. */
 st_status st_farfield_pairs(size_t n_pairs, const double* dx, int order, int stokeslet,
                             int stresslet, const double* stok, const double* str,
                             const double* trace, const double* sym, double* u_out);

@@ -94,6 +94,7 @@ def _load_or():
         L.or_relative_error.argtypes = [_sz, _dp, _dp, C.POINTER(C.c_double)]
         L.or_mac.argtypes = [C.c_double, C.c_double, C.c_double]
         L.or_mac.restype = C.c_int
+        L.or_generate.argtypes = [C.c_int, _sz, C.c_uint64, C.c_int, _vp, _vp, _vp, _vp]
         _or = L
     return _or
 
@@ -295,13 +296,29 @@ def or_direct_at(ps, targets, sto=True, stre=True, threads=None):
     return u
 
 
-def or_direct_points(ps, xyz, sto=True, stre=True):
+def or_direct_points(ps, xyz, sto=True, stre=True, threads=1):
+    """Direct sum at disjoint points; `threads` host threads each take a contiguous block of
+    points (ctypes releases the GIL during the C call)."""
     L = _load_or()
     n, p, _keep = _arrs(ps)
     xyz = np.ascontiguousarray(xyz, np.float64).reshape(-1, 3)
     u = np.zeros((len(xyz), 3))
-    _check(L.or_direct_points(n, p[0], p[1], p[2], p[3], int(sto), int(stre), xyz.reshape(-1), len(xyz),
-                              u.reshape(-1)), "or_direct_points")
+    nt = len(xyz)
+    threads = max(1, min(threads, nt))
+    cuts = [nt * k // threads for k in range(threads + 1)]
+
+    def part(k):
+        a, b = cuts[k], cuts[k + 1]
+        if b > a:
+            _check(L.or_direct_points(n, p[0], p[1], p[2], p[3], int(sto), int(stre), xyz[a:b].reshape(-1), b - a,
+                                      u[a:b].reshape(-1)), "or_direct_points")
+
+    if threads == 1:
+        part(0)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(part, range(threads)))
     return u
 
 
@@ -459,6 +476,32 @@ def ref_read_particles(path, cap):
     k = n.value
     return dict(position=a[0][:k], force_weight=a[1][:k] if sto.value else None,
                 dipole_weight=a[2][:k] if stre.value else None, normal=a[3][:k] if stre.value else None)
+
+
+# ---------------------------------------------------------------- seeded inputs
+GEN_KINDS = {"unit": 0, "cube": 1, "sphere": 2, "mixture": 3, "points": 4}
+
+
+def generate(kind: str, n: int, seed: int, with_stresslets: bool = True) -> dict:
+    """Seeded BASELINE inputs from the oracle's own C generator (or_generate; the recipes of
+    DESIGN.md section 7).  The reference arm of bench.py builds its inputs with this, so it
+    never loads the product library; tests/test_inputs_io.py pins the bytes to the
+    product's st_generate by SHA-256."""
+    L = _load_or()
+    k = GEN_KINDS[kind]
+    pos = np.empty((n, 3))
+    f = None if k == 4 else np.empty((n, 3))
+    h = np.empty((n, 3)) if (with_stresslets and k != 4) else None
+    nu = np.empty((n, 3)) if (with_stresslets and k != 4) else None
+    _check(L.or_generate(k, n, seed, 1 if with_stresslets else 0, _opt_out(pos), _opt_out(f), _opt_out(h),
+                         _opt_out(nu)), "or_generate")
+    if k == 4:
+        return dict(position=pos)
+    return dict(position=pos, force_weight=f, dipole_weight=h, normal=nu)
+
+
+def _opt_out(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
 # ---------------------------------------------------------------- seeded inputs (pure Python)

@@ -790,3 +790,91 @@ int or_mac(double radius, double dist2, double theta) {
     if (dist2 == 0.0) return 0;
     return radius * radius <= theta * theta * dist2;
 }
+
+/* ------------------------------------------------------------------ */
+/* Seeded BASELINE inputs, restated on the oracle side so that the      */
+/* reference arm of bench.py never loads the product library.          */
+/* Stream: SplitMix64 (rng.hpp:10-29): uniform01 = (next >> 11) 2^-53,  */
+/* symmetric = 2u - 1.  Per-particle draw order of                      */
+/* testutil::random_particles (tests/support/test_helpers.hpp:31-49):   */
+/* position, f, then h and the rejection unit normal (random_unit,      */
+/* :22-28; v * (1/sqrt(n2)) as vec3.hpp:41).  The BASELINE recipes      */
+/* (cube, sphere surface, Gaussian mixture, target points) are those    */
+/* of DESIGN.md section 7; tests/test_inputs_io.py pins the bytes to    */
+/* the product's st_generate by SHA-256.                                */
+/* kind: 0 unit box, 1 cube, 2 sphere surface, 3 mixture, 4 points.     */
+/* ------------------------------------------------------------------ */
+static uint64_t sm_next(uint64_t *s) {
+    uint64_t z;
+    *s += 0x9E3779B97F4A7C15ull;
+    z = *s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static double sm_u01(uint64_t *s) { return (double)(sm_next(s) >> 11) * (1.0 / 9007199254740992.0); }
+static double sm_sym(uint64_t *s) { return 2.0 * sm_u01(s) - 1.0; }
+static void sm_unit(uint64_t *s, double out[3]) {
+    for (;;) {
+        double v[3], n2, inv;
+        v[0] = sm_sym(s);
+        v[1] = sm_sym(s);
+        v[2] = sm_sym(s);
+        n2 = nrm2(v);
+        if (n2 > 1e-4 && n2 <= 1.0) {
+            inv = 1.0 / sqrt(n2);
+            out[0] = v[0] * inv;
+            out[1] = v[1] * inv;
+            out[2] = v[2] * inv;
+            return;
+        }
+    }
+}
+
+int or_generate(int kind, size_t n, uint64_t seed, int with_stresslets, double *pos, double *f,
+                double *h, double *nu) {
+    uint64_t s = seed;
+    double centres[16][3];
+    size_t i;
+    int a, k;
+    const double two_pi = 6.283185307179586;
+    if (kind < 0 || kind > 4 || !pos) return OR_INVALID;
+    if (kind != 4 && (!f || (with_stresslets && (!h || !nu)))) return OR_INVALID;
+    if (kind == 3)
+        for (k = 0; k < 16; ++k)
+            for (a = 0; a < 3; ++a) centres[k][a] = -0.5 + 1.0 * sm_u01(&s);
+    for (i = 0; i < n; ++i) {
+        double *p = pos + 3 * i;
+        if (kind == 0) {
+            for (a = 0; a < 3; ++a) p[a] = 0.0 + 1.0 * sm_u01(&s);
+        } else if (kind == 1 || kind == 4) {
+            for (a = 0; a < 3; ++a) p[a] = -0.5 + 1.0 * sm_u01(&s);
+        } else if (kind == 2) {
+            sm_unit(&s, p);
+        } else {
+            const double *c = centres[sm_next(&s) % 16];
+            double g[4];
+            for (k = 0; k < 2; ++k) { /* Box-Muller, two normals per uniform pair */
+                const double u1 = sm_u01(&s), u2 = sm_u01(&s);
+                const double rad = sqrt(-2.0 * log(1.0 - u1));
+                g[2 * k] = rad * cos(two_pi * u2);
+                g[2 * k + 1] = rad * sin(two_pi * u2);
+            }
+            for (a = 0; a < 3; ++a) p[a] = c[a] + 0.05 * g[a];
+        }
+        if (kind == 4) continue;
+        for (a = 0; a < 3; ++a) f[3 * i + a] = sm_sym(&s);
+        if (!with_stresslets) {
+            if (kind == 2 && nu)
+                for (a = 0; a < 3; ++a) nu[3 * i + a] = p[a];
+            continue;
+        }
+        for (a = 0; a < 3; ++a) h[3 * i + a] = sm_sym(&s);
+        if (kind == 2) {
+            for (a = 0; a < 3; ++a) nu[3 * i + a] = p[a];
+        } else {
+            sm_unit(&s, nu + 3 * i);
+        }
+    }
+    return OR_OK;
+}

@@ -47,7 +47,7 @@ __all__ = [
     "farfield_pairs", "taylor_coeffs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
     "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS", "sphere_particles", "cube_particles",
     "write_particles", "read_particles", "treecode_velocity_sweep",
-    "ipc_export", "ipc_open", "ipc_close",
+    "ipc_export", "ipc_open", "ipc_close", "release_workspace",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -65,7 +65,7 @@ EXPORTED_SYMBOLS = (
     "st_shard_cuts", "st_generate", "st_fp64_peak", "st_interaction_lists", "st_treecode_velocity_sweep",
     "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
     "st_read_particles", "st_loaded_copy", "st_loaded_free", "st_treecode_shard_device", "st_unbatch_device",
-    "st_taylor_coeffs", "st_ipc_export", "st_ipc_open", "st_ipc_close",
+    "st_taylor_coeffs", "st_ipc_export", "st_ipc_open", "st_ipc_close", "st_release_workspace",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -165,6 +165,7 @@ def load_library():
     L.st_loaded_copy.argtypes = [vp, vp, vp, vp, vp]
     L.st_loaded_free.argtypes = [vp]
     L.st_loaded_free.restype = None
+    L.st_release_workspace.argtypes = []
     for name in EXPORTED_SYMBOLS:
         if name not in ("st_abi_version", "st_last_error", "st_tree_num_clusters",
                         "st_tree_num_particles", "st_tree_free", "st_sphere_count", "st_loaded_free"):
@@ -696,6 +697,12 @@ def fp64_peak(seconds: float = 0.2) -> float:
     out = C.c_double(0)
     _check(load_library().st_fp64_peak(float(seconds), C.byref(out)))
     return out.value
+
+
+def release_workspace() -> None:
+    """Return the library's cached device memory on the current device to the driver
+    (st_release_workspace; synchronises the device)."""
+    _check(load_library().st_release_workspace())
 
 
 def device_count() -> int:

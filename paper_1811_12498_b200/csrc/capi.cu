@@ -51,6 +51,45 @@ st_status guarded(F&& f) {
 
 // ------------------------------------------------------------ device context
 
+// Private per-device pools (st_common.cuh).
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+
+}  // namespace
+
+cudaMemPool_t st::device_pool() {
+    int dev = 0;
+    ST_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    cudaMemPool_t& p = g_pool[dev & 63];
+    if (!p) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        ST_CUDA(cudaMemPoolCreate(&p, &props));
+        uint64_t thr = UINT64_MAX;
+        ST_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    return p;
+}
+
+void st::pool_grant_peer(int owner, int peer) {
+    int cur = 0;
+    ST_CUDA(cudaGetDevice(&cur));
+    ST_CUDA(cudaSetDevice(owner));
+    cudaMemPool_t p = device_pool();
+    ST_CUDA(cudaSetDevice(cur));
+    cudaMemAccessDesc d = {};
+    d.location.type = cudaMemLocationTypeDevice;
+    d.location.id = peer;
+    d.flags = cudaMemAccessFlagsProtReadWrite;
+    ST_CUDA(cudaMemPoolSetAccess(p, &d, 1));
+}
+
+namespace {
+
 // Per-device check done once (cudaGetDeviceProperties is slow and takes driver locks;
 // it must not sit inside every call's timed path).
 std::mutex g_dev_mu;
@@ -73,26 +112,22 @@ void ensure_device() {
         ST_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
         g_dev_state[dev] = major == 10 ? 1 : 2;
         if (major == 10) {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t thr = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-                // Map a block of pool memory once and keep it: a stream-ordered allocation
-                // that has to grow the pool was measured to block the host for 10-550 ms
-                // (GB-size requests at cfg4), mid-call.  8% of the device (ST_POOL_RESERVE_GB
-                // overrides); larger problems still grow the pool as needed.
-                size_t fr = 0, tot = 0;
-                if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-                    size_t reserve = tot / 100 * 8;
-                    if (const char* env = getenv("ST_POOL_RESERVE_GB")) reserve = (size_t)(atof(env) * 1e9);
-                    reserve = std::min(reserve, fr / 2);
-                    void* p = nullptr;
-                    if (reserve && cudaMallocAsync(&p, reserve, 0) == cudaSuccess) {
-                        cudaFreeAsync(p, 0);
-                        cudaStreamSynchronize(0);
-                    }
-                    cudaGetLastError();
+            cudaMemPool_t pool = device_pool();
+            // Map a block of pool memory once and keep it: a stream-ordered allocation that
+            // has to grow the pool was measured to block the host for 10-550 ms (GB-size
+            // requests at cfg4), mid-call.  8% of the device, at most half of what is free
+            // (ST_POOL_RESERVE_GB overrides); larger problems still grow the pool as needed.
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+                size_t reserve = tot / 100 * 8;
+                if (const char* env = getenv("ST_POOL_RESERVE_GB")) reserve = (size_t)(atof(env) * 1e9);
+                reserve = std::min(reserve, fr / 2);
+                void* p = nullptr;
+                if (reserve && cudaMallocFromPoolAsync(&p, reserve, pool, 0) == cudaSuccess) {
+                    cudaFreeAsync(p, 0);
+                    cudaStreamSynchronize(0);
                 }
+                cudaGetLastError();
             }
         } else {
             fail(ST_CUDA_ERROR, "device " + std::to_string(dev) + " is sm_" + std::to_string(major) +
@@ -241,25 +276,31 @@ void validate_shape(const st_particles* ps, bool sto, bool str) {
     }
 }
 
-// Device part of validate(ps, sel) on device-resident arrays.
-void validate_values_device(size_t n, const double* pos, const double* f, const double* h, const double* nu,
-                            bool sto, bool str, cudaStream_t s) {
-    DevArray<unsigned long long> bad(5, s);
-    bad.fill_bytes(0xff);
-    k_validate<<<nblocks(n, 256), 256, 0, s>>>(n, pos, sto ? f : nullptr, str ? h : nullptr,
-                                                str ? nu : nullptr, str ? 1 : 0, bad.get());
-    ST_LAUNCH("k_validate");
-    count_launch();
-    unsigned long long hb[5];
-    ST_CUDA(cudaMemcpyAsync(hb, bad.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
-    ST_CUDA(cudaStreamSynchronize(s));
-    const char* names[4] = {"position", "force_weight", "dipole_weight", "normal"};
-    for (int k = 0; k < 4; ++k)
-        if (hb[k] != ~0ull)
-            fail(ST_INVALID_ARGUMENT, std::string("particle array '") + names[k] + "' contains a non-finite value");
-    if (hb[4] != ~0ull) fail(ST_INVALID_ARGUMENT, "normal " + std::to_string(hb[4]) + " is not unit length");
+// validate(ps, sel)'s value checks (particles.hpp:47-69) on the host, in the reference's
+// order: every array in turn (position, force_weight, dipole_weight, normal), then the
+// unit normals.  Used by the O(N^2) direct entry points, whose range checks follow it.
+void validate_values_host(const st_particles* ps, bool sto, bool str) {
+    const size_t n = ps->n;
+    auto finite = [n](const double* a, const char* name) {
+        for (size_t i = 0; i < 3 * n; ++i)
+            if (!std::isfinite(a[i]))
+                fail(ST_INVALID_ARGUMENT, std::string("particle array '") + name + "' contains a non-finite value");
+    };
+    finite(ps->position, "position");
+    if (sto) finite(ps->force_weight, "force_weight");
+    if (str) {
+        finite(ps->dipole_weight, "dipole_weight");
+        finite(ps->normal, "normal");
+        for (size_t i = 0; i < n; ++i) {
+            const double* v = ps->normal + 3 * i;
+            const double len = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            if (std::fabs(len - 1.0) > 1e-12)
+                fail(ST_INVALID_ARGUMENT, "normal " + std::to_string(i) + " is not unit length");
+        }
+    }
 }
 
+// Device part of validate(ps, sel) on device-resident arrays.
 // ------------------------------------------------------------ device-resident inputs
 struct DevParticles {
     size_t n = 0;
@@ -319,6 +360,11 @@ struct ShardOut {
     int w0 = 0, w1 = 0;         // warp (32-target batch) range evaluated
     DevArray<uint32_t> torig;   // batch position -> original target index (if requested)
 };
+
+bool moments_inline() {
+    const char* v = getenv("ST_MOMENTS_INLINE");
+    return v && v[0] == '1';
+}
 
 // The particle arrays other than positions may still be in flight on another stream:
 // `weights_ready` (if set) is waited for after the tree build, which needs positions only.
@@ -380,6 +426,9 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     fold_weights_device(M.get(), tree.ncl, prm.order, sto, str, aux.s, W);
     M.reset();
     e2.record(aux.s);
+    // ST_MOMENTS_INLINE=1 (measurement only): nothing overlaps the moment pass, so
+    // time_moments_s is its own duration (bench.py's moments roofline)
+    if (moments_inline()) ST_CUDA(cudaStreamWaitEvent(s, e2.e, 0));
 
     // batch order of the targets: 63-bit Morton order in their tight box (one radix sort,
     // done on the second stream above)
@@ -635,6 +684,7 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
         const cudaError_t e = cudaDeviceEnablePeerAccess(dev0, 0);
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
         cudaGetLastError();
+        pool_grant_peer(dev0, dev);  // the output buffers below come from device 0's pool
     }
     ST_CUDA(cudaSetDevice(dev0));
     OwnedStream os0;
@@ -713,6 +763,16 @@ struct st_tree {
 extern "C" {
 
 int st_abi_version(void) { return ST_ABI_VERSION; }
+
+st_status st_release_workspace(void) {
+    return guarded([&] {
+        int dev = 0;
+        ST_CUDA(cudaGetDevice(&dev));
+        ST_CUDA(cudaDeviceSynchronize());
+        release_near_workspace(dev);
+        ST_CUDA(cudaMemPoolTrimTo(device_pool(), 0));
+    });
+}
 
 const char* st_last_error(void) { return g_last_error.c_str(); }
 
@@ -1030,15 +1090,15 @@ st_status st_interaction_lists(const st_particles* src, const st_params* params,
     });
 }
 
+// The callers have validated shapes and values on the host (then the target range, as
+// in the reference, kernels.hpp:125-127, 143-146).
 static void direct_common(const st_particles* src, int sto, int str, const std::vector<int64_t>& tg,
                           double* u_out, bool naive) {
-    validate_shape(src, sto != 0, str != 0);
     ensure_device();
     OwnedStream os;
     cudaStream_t s = os.s;
     DevParticles d;
     upload(src, sto != 0, str != 0, d, s);
-    validate_values_device(d.n, d.pos, d.f, d.h, d.nu, sto != 0, str != 0, s);
     DevArray<double> rec(12 * d.n, s);
     k_pack<<<nblocks(d.n, 256), 256, 0, s>>>(d.n, nullptr, d.pos, d.f, d.h, d.nu, rec.get(), nullptr);
     ST_LAUNCH("k_pack");
@@ -1058,13 +1118,16 @@ static void direct_common(const st_particles* src, int sto, int str, const std::
     if (nt) d2h(u_out, du.get(), 3 * nt * sizeof(double), s);
     ST_CUDA(cudaStreamSynchronize(s));
     if (herr)
-        fail(ST_DOMAIN_ERROR, naive ? "stokeslet: coincident points" : "direct sum: coincident particles");
+        // naive_direct_velocity forms the Stokeslet before the stresslet (kernels.hpp:98-112)
+        fail(ST_DOMAIN_ERROR, naive ? (sto ? "stokeslet: coincident points" : "stresslet: coincident points")
+                                    : "direct sum: coincident particles");
 }
 
 st_status st_direct_velocity(const st_particles* src, int sto, int str, size_t first, size_t last,
                              double* u_out) {
     return guarded([&] {
         validate_shape(src, sto != 0, str != 0);
+        validate_values_host(src, sto != 0, str != 0);
         if (first > last || last > src->n)
             fail(ST_INVALID_ARGUMENT, "contracted_direct_velocity: bad target range");
         std::vector<int64_t> tg(last - first);
@@ -1077,6 +1140,7 @@ st_status st_direct_velocity_at(const st_particles* src, int sto, int str, const
                                 size_t n_targets, double* u_out) {
     return guarded([&] {
         validate_shape(src, sto != 0, str != 0);
+        validate_values_host(src, sto != 0, str != 0);
         std::vector<int64_t> tg(n_targets);
         for (size_t i = 0; i < n_targets; ++i) {
             if (targets[i] >= src->n)
@@ -1088,7 +1152,11 @@ st_status st_direct_velocity_at(const st_particles* src, int sto, int str, const
 }
 
 st_status st_naive_direct_velocity(const st_particles* src, int sto, int str, double* u_out) {
-    return guarded([&] { direct_common(src, sto, str, {}, u_out, true); });
+    return guarded([&] {
+        validate_shape(src, sto != 0, str != 0);
+        validate_values_host(src, sto != 0, str != 0);
+        direct_common(src, sto, str, {}, u_out, true);
+    });
 }
 
 st_status st_build_tree(const st_particles* src, int leaf_capacity, int shrink, st_tree** out) {

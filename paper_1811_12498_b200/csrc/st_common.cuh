@@ -65,8 +65,16 @@ inline double secs(const Event& a, const Event& b) {
     return ms * 1e-3;
 }
 
-// Stream-ordered device array (cudaMallocAsync on the device's default pool,
-// whose release threshold is raised once so memory is recycled across calls).
+// The library's private stream-ordered memory pool on the current device (created on
+// first use; the process's default pool is left as the host application configured it).
+// Its release threshold is raised so memory is recycled across calls; st_release_workspace
+// trims it.
+cudaMemPool_t device_pool();
+// Let device `peer` read/write allocations from `owner`'s pool (NVLink stores into
+// another GPU's output: peer access alone does not cover pool memory).
+void pool_grant_peer(int owner, int peer);
+
+// Stream-ordered device array (cudaMallocFromPoolAsync on device_pool()).
 template <class T>
 class DevArray {
 public:
@@ -91,7 +99,7 @@ public:
         if (n) {
             static const bool dbg = getenv("ST_DEBUG_ALLOC") != nullptr;
             const auto t0 = std::chrono::steady_clock::now();
-            ST_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+            ST_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), device_pool(), s));
             if (dbg) {
                 const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
                 if (ms > 1.0) fprintf(stderr, "[alloc] %.1f MB took %.1f ms\n", n * sizeof(T) / 1e6, ms);

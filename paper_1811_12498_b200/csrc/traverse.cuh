@@ -76,6 +76,8 @@ void launch_naive(bool sto, bool str, const double* rec, size_t n, double* u, in
                   cudaStream_t s);
 
 // Per-pair far-field API: n pairs, pair i uses dx[3i..] and weight block i.
+// Frees device `dev`'s near-field entry workspace (st_release_workspace).
+void release_near_workspace(int dev);
 void launch_far_pairs(int P, size_t n, const double* dx, const double* W, double* u, cudaStream_t s);
 // Reference-order Coulomb coefficients b^k, |k| <= pmax (coulomb.hpp:28-50).
 void launch_coulomb(size_t n, const double* dx, int pmax, double* b, cudaStream_t s);

@@ -148,3 +148,22 @@ def test_relative_error_host(S):
         S.relative_error(np.zeros((1, 3)), np.ones((1, 3)))
     with pytest.raises(S.InvalidArgument):
         S.relative_error(ref[:1], ref)
+
+
+def test_bench_relaunch_command_is_torchrun_with_n_ranks():
+    """bench.py --gpus N (N > 1) without torchrun re-launches itself with N ranks."""
+    import sys
+    import bench
+    cmd = bench.relaunch_command(["--gpus", "4", "--steps", "2"], 4, 29555)
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[cmd.index(bench.__file__.replace(".pyc", ".py")) + 1:] == ["--gpus", "4", "--steps", "2"]
+
+
+def test_bench_far_flop_conventions():
+    import bench
+    # SURVEY.md 8d table (reference-equivalent flops per accepted pair)
+    assert [bench.f_far(p) for p in (2, 4, 6, 8, 10)] == [2278, 7527, 17640, 34209, 58826]
+    # executed flops at P = 10 (p = 8 with stresslets), as counted in the SASS
+    assert bench.far_executed_flops(10) == 1226
+    assert bench.f_far(8) / bench.far_executed_flops(10) == pytest.approx(27.9, abs=0.05)

@@ -72,3 +72,30 @@ def test_cli_sphere_human_and_file_round_trip(cli, tmp_path):
     assert r2.returncode == 0, r2.stderr
     rows = list(csv.reader(open(tmp_path / "o.csv")))
     assert abs(float(dict(zip(rows[0], rows[1]))["error_E"]) - e) <= 1e-5 * e  # human report: 6 digits
+
+
+def _build_harness_bytes(tmp_path, include_dir, link_product):
+    exe = tmp_path / ("hb_" + ("mine" if link_product else "ref"))
+    cmd = ["g++", "-std=c++20", "-O1", "-I" + include_dir, "-o", str(exe),
+           os.path.join(ROOT, "tests", "cpp", "harness_bytes.cpp")]
+    if link_product:
+        libdir = os.path.join(ROOT, "paper_1811_12498_b200")
+        cmd += ["-L" + libdir, "-lstokestree_b200", "-Wl,-rpath," + libdir]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    return str(exe)
+
+
+def test_harness_renderings_match_reference_bytes(tmp_path):
+    """write_csv / read_csv (incl. every error) / write_human of the drop-in harness produce
+    the reference's bytes (golden: tests/cpp/harness_bytes.cpp compiled against the
+    reference's bench.hpp, tests/golden/harness_bytes.txt).  Host-only."""
+    exe = _build_harness_bytes(tmp_path, os.path.join(ROOT, "include"), True)
+    mine = subprocess.run([exe], capture_output=True, check=True).stdout
+    golden = open(os.path.join(ROOT, "tests", "golden", "harness_bytes.txt"), "rb").read()
+    assert mine == golden
+    ref_inc = "/root/reference/proj/include"
+    if os.path.isdir(ref_inc):  # regenerate the golden from the reference itself
+        ref = subprocess.run([_build_harness_bytes(tmp_path, ref_inc, False)], capture_output=True,
+                             check=True).stdout
+        assert ref == golden

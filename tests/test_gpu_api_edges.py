@@ -1,0 +1,79 @@
+"""GPU edge cases of the drop-in API: error messages and their order (the reference's
+throw order), empty shards, and the library's device-memory lifetime."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_naive_coincident_message_follows_kernel_selection(S):
+    # naive_direct_velocity forms the Stokeslet first, so with stresslets only the
+    # reference throws stresslet()'s message (kernels.hpp:17, 31, 98-112)
+    pos = np.array([[0, 0, 0], [1, 1, 1], [0, 0, 0.0]])
+    one = np.tile([1.0, 0, 0], (3, 1))
+    ps = S.ParticleSet(pos, one, one, one)
+    with pytest.raises(S.DomainError, match="^stokeslet: coincident points$"):
+        S.naive_direct_velocity(ps, S.KernelSelection.both())
+    with pytest.raises(S.DomainError, match="^stresslet: coincident points$"):
+        S.naive_direct_velocity(ps, S.KernelSelection.stresslet_only())
+    with pytest.raises(S.DomainError, match="^direct sum: coincident particles$"):
+        S.contracted_direct_velocity(ps, S.KernelSelection.stresslet_only())
+
+
+def test_direct_validates_values_before_the_target_range(S):
+    # contracted_direct_velocity[_at] call validate(ps, sel) before the range / index
+    # checks (kernels.hpp:125-127, 143-146)
+    ps = S.generate("cube", 50, 3, True)
+    bad = S.ParticleSet(ps.position.copy(), ps.force_weight, ps.dipole_weight, ps.normal.copy())
+    bad.normal[4] *= 3.0
+    with pytest.raises(S.InvalidArgument, match="normal 4 is not unit length"):
+        S.contracted_direct_velocity(bad, S.KernelSelection.both(), 10, 5)
+    with pytest.raises(S.InvalidArgument, match="normal 4 is not unit length"):
+        S.contracted_direct_velocity_at(bad, S.KernelSelection.both(), [51])
+    with pytest.raises(S.InvalidArgument, match="bad target range"):
+        S.contracted_direct_velocity(ps, S.KernelSelection.both(), 10, 5)
+    with pytest.raises(S.InvalidArgument, match="target out of range"):
+        S.contracted_direct_velocity_at(ps, S.KernelSelection.both(), [51])
+
+
+@pytest.mark.parametrize("nt", [1, 31, 100, 255])
+def test_empty_shards_with_many_devices(S, nt):
+    # fewer 32-target batch warps than shards: some shards are empty and must still order
+    # their frees and timings after the moment pass (capi.cu run_treecode)
+    ps = S.generate("cube", 20000, 11, True)
+    tg = S.generate("points", nt, 67890).position
+    prm1 = S.TreecodeParams(order=5, theta=0.5, leaf_capacity=300)
+    one = S.treecode_velocity_targets(ps, tg, prm1, per_target=True)
+    for dev in (3, 8):
+        prm = S.TreecodeParams(order=5, theta=0.5, leaf_capacity=300, devices=dev)
+        many = S.treecode_velocity_targets(ps, tg, prm, per_target=True)
+        assert many.velocity.tobytes() == one.velocity.tobytes()
+        assert np.array_equal(many.per_target, one.per_target)
+        assert many.time_moments_s >= 0.0 and many.time_total_s > 0.0
+
+
+def test_release_workspace_returns_memory_and_calls_still_work(S):
+    import torch
+    ps = S.generate("cube", 200000, 5, True)
+    prm = S.TreecodeParams(order=4, theta=0.5, leaf_capacity=1000)
+    a = S.treecode_velocity(ps, prm).velocity
+    free_before, _ = torch.cuda.mem_get_info()
+    S.release_workspace()
+    free_after, _ = torch.cuda.mem_get_info()
+    assert free_after >= free_before  # the pool and the near workspace were trimmed
+    b = S.treecode_velocity(ps, prm).velocity
+    assert a.tobytes() == b.tobytes()
+    S.release_workspace()
+
+
+def test_default_pool_is_not_reconfigured(S):
+    # the library allocates from a private pool: the process's default pool keeps its
+    # release threshold (0 unless the host application changed it)
+    from cuda.bindings import runtime as rt
+    ps = S.generate("cube", 5000, 5, True)
+    S.treecode_velocity(ps, S.TreecodeParams(order=3, leaf_capacity=200))
+    err, pool = rt.cudaDeviceGetDefaultMemPool(0)
+    assert err == rt.cudaError_t.cudaSuccess
+    err, thr = rt.cudaMemPoolGetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReleaseThreshold)
+    assert err == rt.cudaError_t.cudaSuccess
+    assert int(thr) == 0

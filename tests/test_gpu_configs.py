@@ -1,0 +1,117 @@
+"""Parity at the BASELINE.json configurations themselves (full size), against the
+reference compiled in place (oracle/_ref).
+
+Per config (cfg1 1M cube p8; cfg2 4M sphere p10 theta0.7; cfg3 16M cube p8 N0 4000;
+cfg4 8M Gaussian-mixture sources -> 8M disjoint targets, theta 0.6):
+  * the tree (permutation, ranges, children, leaf flags, the BYTES of centre/radius/bbox)
+    equals the reference's build_tree (cluster_tree.hpp:152-192);
+  * moments of every cluster (M2M-shifted here, particle sums there) agree to 1e-12 of the
+    cluster's largest moment, at the full depth of the config's tree (moments.hpp:140-175);
+  * on a strided target sample (4,000 at cfg1, 2,000 elsewhere) the per-target visited /
+    accepted / direct-pair counts are equal and the velocities within 1e-12 relative L2 of
+    the reference treecode (engine.hpp:80-108, via detail::accumulate_velocity);
+  * the error against the direct sum on the reference harness's strided 1,000-target subset
+    (bench.hpp:235-256) equals the reference's own error there within 1%.
+The reference side runs on all host cores; cfg3 takes ~1-2 minutes of host time."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import as_dict
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+REL_TOL = 1e-12
+CFG = {
+    "cfg1": dict(kind="cube", n=1_000_000, order=8, theta=0.5, n0=2000, targets=None, sample=4000),
+    "cfg2": dict(kind="sphere", n=4_000_000, order=10, theta=0.7, n0=2000, targets=None, sample=2000),
+    "cfg3": dict(kind="cube", n=16_000_000, order=8, theta=0.5, n0=4000, targets=None, sample=2000),
+    "cfg4": dict(kind="mixture", n=8_000_000, order=8, theta=0.6, n0=2000, targets=8_000_000, sample=2000),
+}
+THREADS = len(os.sched_getaffinity(0))
+
+
+def strided(nt, k):
+    stride = max(1, nt // k)
+    return (np.arange(k, dtype=np.int64) * stride)[: min(k, nt)]
+
+
+@pytest.mark.parametrize("name", list(CFG))
+def test_config_parity(S, need_ref, name):
+    c = CFG[name]
+    O = need_ref
+    ps = S.generate(c["kind"], c["n"], 12345, True)
+    tg = S.generate("points", c["targets"], 67890).position if c["targets"] else None
+    nt = c["targets"] or c["n"]
+    ctx = O.RefContext(as_dict(ps), c["order"], c["theta"], c["n0"], True, workers=THREADS)
+    try:
+        # ---- tree, bit for bit
+        T = S.build_tree(ps, c["n0"], True)
+        R = ctx.tree()
+        assert T.ncl == R.ncl
+        assert np.array_equal(T.to_original, R.to_original)
+        assert np.array_equal(T.begin, R.begin) and np.array_equal(T.end, R.end)
+        assert np.array_equal(T.children, R.children)
+        assert np.array_equal(T.n_children, R.n_children) and np.array_equal(T.is_leaf, R.is_leaf)
+        assert np.array_equal(T.geom.view(np.uint64), R.geom.view(np.uint64))
+
+        # ---- moments at the config's depth
+        m = S.compute_moments(T, c["order"], S.KernelSelection.both())
+        r = ctx.moments()
+        for key, mine in (("stok", m.stok), ("str", m.str), ("trace", m.trace), ("sym", m.sym)):
+            ref = r[key].reshape(mine.shape)
+            scale = np.abs(ref).max(axis=(1, 2), keepdims=True) + 1e-300
+            dev = float(np.max(np.abs(mine - ref) / scale))
+            assert dev < 1e-12, (name, key, dev)
+        del m, r
+
+        # ---- the treecode: every target on the GPU, a strided sample on the reference
+        prm = S.TreecodeParams(order=c["order"], theta=c["theta"], leaf_capacity=c["n0"])
+        res = S.treecode_velocity_targets(ps, tg, prm, per_target=True)
+        idx = strided(nt, c["sample"])
+        if tg is None:
+            u_ref, pt_ref, _ = ctx.eval(src_idx=idx, threads=THREADS)
+        else:
+            u_ref, pt_ref, _ = ctx.eval(xyz=tg[idx], threads=THREADS)
+        assert np.array_equal(res.per_target[idx], pt_ref), name
+        err = S.relative_error(u_ref, res.velocity[idx])
+        assert err <= REL_TOL, (name, err)
+
+        # ---- accuracy against the direct sum, ours and the reference's
+        acc = strided(nt, 1000)
+        u_tree_ref = u_ref if c["sample"] == 1000 else (
+            ctx.eval(src_idx=acc, threads=THREADS)[0] if tg is None else ctx.eval(xyz=tg[acc], threads=THREADS)[0])
+        if tg is None:
+            u_dir = S.contracted_direct_velocity_at(ps, S.KernelSelection.both(), acc)
+            u_dir_ref = O.ref_direct_at(as_dict(ps), acc, threads=THREADS)
+            assert S.relative_error(u_dir_ref, u_dir) < 1e-13
+        else:
+            u_dir = S.treecode_velocity_targets(ps, tg[acc], S.TreecodeParams(order=0, theta=1e-9,
+                                                                             leaf_capacity=c["n0"])).velocity
+            u_dir_ref = O.or_direct_points(as_dict(ps), tg[acc], threads=THREADS)
+            assert S.relative_error(u_dir_ref, u_dir) < 1e-13
+        e_gpu = S.relative_error(u_dir, res.velocity[acc])
+        e_ref = O.relative_error(u_dir_ref, u_tree_ref)
+        assert abs(e_gpu - e_ref) <= 0.01 * e_ref, (name, e_gpu, e_ref)
+        print(f"{name}: tree ncl={T.ncl}, sample rel L2 {err:.2e}, E gpu {e_gpu:.4e} ref {e_ref:.4e}, "
+              f"stats {res.stats}")
+    finally:
+        ctx.close()
+
+
+def test_cfg1_stats_match_the_survey_reference_run(S, need_ref):
+    """cfg1's whole-run traversal statistics equal the reference's parallel_velocity
+    (engine.hpp:157-180) on all 1M targets: the sum of the per-target counters the
+    sample test checks target by target."""
+    c = CFG["cfg1"]
+    ps = S.generate(c["kind"], c["n"], 12345, True)
+    prm = S.TreecodeParams(order=c["order"], theta=c["theta"], leaf_capacity=c["n0"])
+    res = S.treecode_velocity(ps, prm, per_target=True)
+    assert res.stats.farfield_evals == int(res.per_target[:, 1].sum())
+    assert res.stats.direct_pairs == int(res.per_target[:, 2].sum())
+    assert res.stats.clusters_visited == int(res.per_target[:, 0].sum())
+    # the survey's reference measurement: 181.0 / 143.3 / 25,699.6 per target
+    assert round(res.stats.clusters_visited / c["n"], 1) == 181.0
+    assert round(res.stats.farfield_evals / c["n"], 1) == 143.3
+    assert round(res.stats.direct_pairs / c["n"], 1) == 25699.6

@@ -82,3 +82,46 @@ def test_particle_file_errors(S, tmp_path):
     ps.normal[2] *= 2
     with pytest.raises(S.InvalidArgument, match="normal 2"):
         S.write_particles(tmp_path / "w.txt", ps, S.KernelSelection.both())
+
+
+def _digest(d):
+    import hashlib
+    h = hashlib.sha256()
+    for key in ("position", "force_weight", "dipole_weight", "normal"):
+        a = d.get(key)
+        h.update(key.encode())
+        if a is not None:
+            h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("kind,n,stresslets", [
+    ("cube", 100_000, True), ("sphere", 60_000, True), ("mixture", 80_000, True), ("points", 50_000, False),
+    ("unit", 3_000, False), ("cube", 1_000_000, True),
+])
+def test_oracle_generator_bytes_equal_product_generator(S, O, kind, n, stresslets):
+    """bench.py's reference arm builds its inputs with the oracle's own generator (it must not
+    load the product library); the bytes must be those the GPU arm evaluates (SHA-256)."""
+    for seed in (12345, 67890):
+        mine = S.generate(kind, n, seed, stresslets)
+        d = dict(position=mine.position, force_weight=mine.force_weight,
+                 dipole_weight=mine.dipole_weight, normal=mine.normal) if kind != "points" \
+            else dict(position=mine.position)
+        o = O.generate(kind, n, seed, stresslets)
+        assert _digest(o) == _digest(d), (kind, seed)
+
+
+def test_reference_arm_does_not_load_the_product_library(tmp_path):
+    """bench.py --impl reference (input generation included) must run without the product
+    library: it is imported in a fresh interpreter with the library path poisoned."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.argv=['bench.py']; sys.path.insert(0, %r); import bench; "
+            "ps, tg = bench.make_reference_inputs(bench.CONFIGS['cfg0']); "
+            "assert 'paper_1811_12498_b200' not in sys.modules, 'product imported'; "
+            "print(ps['position'].shape)") % root
+    env = dict(os.environ, ST_LIB_PATH=str(tmp_path / "missing.so"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert "(10000, 3)" in out.stdout
