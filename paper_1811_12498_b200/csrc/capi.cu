@@ -339,7 +339,8 @@ void raise_flags(const RunOut& ro) {
             fail(ST_INVALID_ARGUMENT, std::string("particle array '") + names[k] + "' contains a non-finite value");
     if (ro.vflags[4] != ~0ull) fail(ST_INVALID_ARGUMENT, "normal " + std::to_string(ro.vflags[4]) + " is not unit length");
     if (ro.vflags[5] != ~0ull) fail(ST_INVALID_ARGUMENT, "targets: non-finite position");
-    if (ro.domain_err) fail(ST_DOMAIN_ERROR, "direct sum: coincident particles");
+    if (ro.domain_err & 2) fail(ST_RUNTIME_ERROR, "MAC accepted a cluster containing the target");
+    if (ro.domain_err & 1) fail(ST_DOMAIN_ERROR, "direct sum: coincident particles");
 }
 
 

@@ -77,3 +77,43 @@ def test_default_pool_is_not_reconfigured(S):
     err, thr = rt.cudaMemPoolGetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReleaseThreshold)
     assert err == rt.cudaError_t.cudaSuccess
     assert int(thr) == 0
+
+
+DEBUG_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1811_12498_b200 as S
+out = []
+for kind, n, n0, theta, disjoint in (("cube", 30000, 200, 0.5, False), ("sphere", 20000, 1, 0.7, False),
+                                     ("mixture", 30000, 100, 0.6, True), ("unit", 5000, 8, 0.9, False)):
+    ps = S.generate(kind, n, 3, True)
+    tg = S.generate("points", 4000, 67890).position if disjoint else None
+    r = S.treecode_velocity_targets(ps, tg, S.TreecodeParams(order=4, theta=theta, leaf_capacity=n0))
+    out.append(r.velocity)
+np.save(sys.argv[2], np.concatenate(out))
+"""
+
+
+def test_debug_build_mac_containment_check(S, tmp_path):
+    """`make debug` compiles the reference's MAC self-containment assert (engine.hpp:88-89) into
+    the walk kernel (ST_DEBUG_CHECKS; a violation fails the call with ST_RUNTIME_ERROR).  The
+    debug library runs clean on trees down to N0 = 1 and theta up to 0.9, bit-identical to
+    the release library."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dbg = os.path.join(root, "paper_1811_12498_b200", "libstokestree_b200_debug.so")
+    if not os.path.exists(dbg):
+        pytest.skip("debug library not built (make -C paper_1811_12498_b200 debug)")
+    res = {}
+    for tag, lib in (("release", None), ("debug", dbg)):
+        env = dict(os.environ)
+        if lib:
+            env["ST_LIB_PATH"] = lib
+        f = tmp_path / f"{tag}.npy"
+        out = subprocess.run([sys.executable, "-c", DEBUG_SCRIPT, root, str(f)], env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr
+        res[tag] = np.load(f)
+    assert res["debug"].tobytes() == res["release"].tobytes()

@@ -85,12 +85,12 @@ def test_config_parity(S, need_ref, name):
         if tg is None:
             u_dir = S.contracted_direct_velocity_at(ps, S.KernelSelection.both(), acc)
             u_dir_ref = O.ref_direct_at(as_dict(ps), acc, threads=THREADS)
-            assert S.relative_error(u_dir_ref, u_dir) < 1e-13
+            assert S.relative_error(u_dir_ref, u_dir) < 1e-12  # 4M-16M-term sums in another order
         else:
             u_dir = S.treecode_velocity_targets(ps, tg[acc], S.TreecodeParams(order=0, theta=1e-9,
                                                                              leaf_capacity=c["n0"])).velocity
             u_dir_ref = O.or_direct_points(as_dict(ps), tg[acc], threads=THREADS)
-            assert S.relative_error(u_dir_ref, u_dir) < 1e-13
+            assert S.relative_error(u_dir_ref, u_dir) < 1e-12  # 4M-16M-term sums in another order
         e_gpu = S.relative_error(u_dir, res.velocity[acc])
         e_ref = O.relative_error(u_dir_ref, u_tree_ref)
         assert abs(e_gpu - e_ref) <= 0.01 * e_ref, (name, e_gpu, e_ref)

@@ -643,3 +643,49 @@ def test_device_call_with_weights_in_flight(S):
                                stream=main.cuda_stream, weights_event=ready.cuda_event)
     torch.cuda.synchronize()
     assert out.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("kind,n,n0,order,theta,world,disjoint", [
+    ("cube", 20000, 300, 4, 0.5, 3, False), ("mixture", 12000, 200, 6, 0.6, 4, True),
+    ("sphere", 9000, 150, 3, 0.7, 2, False),
+])
+def test_shard_plan_matches_host_model(S, O, kind, n, n0, order, theta, world, disjoint):
+    """The batch order (Morton) and the work-balanced shard ranges the library computes on the
+    GPU equal tests/shard_model.py's host restatement (which tests/test_multirank.py uses for
+    its gloo ranks): Morton keys, k_count's float32 cost model, st_shard_cuts."""
+    import torch
+    import shard_model as M
+    ps = S.generate(kind, n, 21, True)
+    tg = S.generate("points", 7000, 67890).position if disjoint else None
+    nt = n if tg is None else len(tg)
+    src = torch.from_numpy(np.concatenate([ps.position, ps.force_weight, ps.dipole_weight, ps.normal])).cuda()
+    b, stride = src.data_ptr(), n * 24
+    ptrs = (b, b + stride, b + 2 * stride, b + 3 * stride)
+    dtg = torch.from_numpy(tg).cuda() if tg is not None else None
+    prm = S.TreecodeParams(order=order, theta=theta, leaf_capacity=n0)
+    stream = torch.cuda.current_stream().cuda_stream
+    torig = torch.empty(nt, dtype=torch.int32, device="cuda")
+    part = torch.zeros((nt, 3), dtype=torch.float64, device="cuda")
+    ranges = []
+    for r in range(world):
+        t0, t1, _ = S.treecode_shard_device(*ptrs, n, prm, part.data_ptr(), torig.data_ptr(),
+                                            targets_ptr=None if dtg is None else dtg.data_ptr(),
+                                            n_targets=0 if dtg is None else nt, shard=r, n_shards=world,
+                                            stream=stream)
+        ranges.append((t0, t1))
+    torch.cuda.synchronize()
+    xyz = ps.position if tg is None else tg
+    order_ = M.morton_batch_order(xyz)
+    assert np.array_equal(torig.cpu().numpy().astype(np.int64), order_)
+    d = as_dict(ps)
+    T = O.or_build_tree(d, n0, True)
+    if tg is None:
+        to_tree = np.empty(n, np.uint32)
+        to_tree[T.to_original] = np.arange(n, dtype=np.uint32)
+        far, near = O.or_lists(d, n0, True, theta, tree_idx=to_tree, cap=8192)
+    else:
+        far, near = O.or_lists(d, n0, True, theta, xyz=tg, cap=8192)
+    cost = M.warp_costs(order_, far, near, (T.end - T.begin), order + 2)
+    cuts = S.shard_cuts(cost, world)
+    want = [(min(nt, 32 * int(cuts[r])), min(nt, 32 * int(cuts[r + 1]))) for r in range(world)]
+    assert ranges == want

@@ -3,9 +3,10 @@
 Every rank derives the same work-balanced cut of the Morton-ordered 32-target
 batches (no communication), owns a disjoint shard, and the batch-order slices
 are all-gathered (bench.allgather_batch_slices) and scattered to original order, so
-the combined result is bit-identical to the single-rank result.  The per-target
-velocities here come from the oracle (no GPU in this container); the CUDA path
-writes the same disjoint-shard layout."""
+the combined result is bit-identical to the single-rank result.  The batch order and the
+cut use the CUDA path's own recipe (tests/shard_model.py: Morton keys, k_count's cost
+model, st_shard_cuts), pinned to the library by a GPU test; the per-target velocities
+here come from the oracle (no GPU in this container)."""
 import os
 import socket
 
@@ -29,35 +30,40 @@ def _free_port():
 def _worker(rank, world, port, q):
     import sys
     sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1811_12498_b200 as S
+    import shard_model as M
     from oracle import oracle as O
-    ps = S.generate("cube", 3000, 12345, True)
+    n, order_p, theta, n0 = 3000, 4, 0.5, 200
+    ps = S.generate("cube", n, 12345, True)
     d = dict(position=ps.position, force_weight=ps.force_weight, dipole_weight=ps.dipole_weight,
              normal=ps.normal)
     # replicated sources: rank 0's copy broadcast to everyone
-    src = torch.from_numpy(ps.position.copy()) if rank == 0 else torch.zeros((3000, 3), dtype=torch.float64)
+    src = torch.from_numpy(ps.position.copy()) if rank == 0 else torch.zeros((n, 3), dtype=torch.float64)
     dist.broadcast(src, 0)
     assert np.array_equal(src.numpy(), ps.position)
-    # batch order = leaf-capacity-32 octree over the targets (same recipe as the CUDA path)
-    order = O.or_build_tree(d, 32, False).to_original.astype(np.int64)
-    nwarps = (len(order) + 31) // 32
-    u_all, _, pt = O.or_treecode(d, 4, 0.5, 200, per_target=True, threads=2)
-    # per-warp cost from the exact per-target counts; identical on every rank
-    cost = np.zeros(nwarps)
-    for w in range(nwarps):
-        tg = order[32 * w:32 * (w + 1)]
-        cost[w] = pt[tg, 1].sum() * 100 + pt[tg, 2].sum()
-    cuts = S.shard_cuts(cost, world)
+    # the CUDA path's batch order (Morton keys in the targets' tight box) and its per-warp
+    # cost model (k_count over the exact interaction lists), restated on the host and checked
+    # against the library by tests/test_gpu_parity.py::test_shard_plan_matches_host_model
+    order = M.morton_batch_order(ps.position)
+    T = O.or_build_tree(d, n0, True)
+    to_tree = np.empty(n, np.uint32)
+    to_tree[T.to_original] = np.arange(n, dtype=np.uint32)
+    far, near = O.or_lists(d, n0, True, theta, tree_idx=to_tree, cap=4096)
+    cost = M.warp_costs(order, far, near, T.end - T.begin, order_p + 2)
+    nwarps = len(cost)
+    cuts = S.shard_cuts(cost, world)  # st_shard_cuts, identical on every rank
+    u_all, _, _ = O.or_treecode(d, order_p, theta, n0, per_target=True, threads=2)
     # this rank's slice in batch order, gathered exactly as bench.py does it
     from bench import allgather_batch_slices
-    t0, t1 = min(3000, 32 * int(cuts[rank])), min(3000, 32 * int(cuts[rank + 1]))
-    ubatch = torch.zeros((3000, 3), dtype=torch.float64)
+    t0, t1 = min(n, 32 * int(cuts[rank])), min(n, 32 * int(cuts[rank + 1]))
+    ubatch = torch.zeros((n, 3), dtype=torch.float64)
     ubatch[t0:t1] = torch.from_numpy(u_all[order[t0:t1]])
     ranges = allgather_batch_slices(dist, ubatch, t0, t1, world)
-    assert ranges[0][0] == 0 and ranges[-1][1] == 3000
-    out = torch.zeros((3000, 3), dtype=torch.float64)
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    out = torch.zeros((n, 3), dtype=torch.float64)
     out[torch.from_numpy(order)] = ubatch  # the unbatch scatter (st_unbatch_device on a GPU)
     allcuts = [torch.zeros(world + 1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(allcuts, torch.from_numpy(cuts))
