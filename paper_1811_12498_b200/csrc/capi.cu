@@ -128,6 +128,11 @@ void ensure_device() {
                     cudaStreamSynchronize(0);
                 }
                 cudaGetLastError();
+                // the near field's entry workspace: 2 GB (65M entries; cfg1 needs 0.6 GB), at
+                // most a tenth of what is free (ST_NEAR_RESERVE_GB overrides)
+                size_t near = std::min<size_t>(2000000000ull, fr / 10);
+                if (const char* env = getenv("ST_NEAR_RESERVE_GB")) near = (size_t)(atof(env) * 1e9);
+                if (near) reserve_near_workspace(dev, near);
             }
         } else {
             fail(ST_CUDA_ERROR, "device " + std::to_string(dev) + " is sm_" + std::to_string(major) +

@@ -76,7 +76,9 @@ void launch_naive(bool sto, bool str, const double* rec, size_t n, double* u, in
                   cudaStream_t s);
 
 // Per-pair far-field API: n pairs, pair i uses dx[3i..] and weight block i.
-// Frees device `dev`'s near-field entry workspace (st_release_workspace).
+// Reserves / frees device `dev`'s near-field entry workspace (ensure_device /
+// st_release_workspace).
+void reserve_near_workspace(int dev, size_t bytes);
 void release_near_workspace(int dev);
 void launch_far_pairs(int P, size_t n, const double* dx, const double* W, double* u, cudaStream_t s);
 // Reference-order Coulomb coefficients b^k, |k| <= pmax (coulomb.hpp:28-50).
