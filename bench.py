@@ -73,37 +73,25 @@ def f_far(p):
 
 def far_executed_flops(P):
     """FP64 flops the far kernels EXECUTE per accepted pair at harmonic order P (= p + 2 with
-    stresslets): far_eval_t<P> in csrc/far_eval.cuh counted op by op (FMA = 2) plus the pair's
-    geometry in the calling loop (dx: 3 DADD; r^2 as the MAC computes it, 3 DMUL + 2 DADD;
-    the accumulation, 3 DADD).  tests/test_sass_counts.py checks this against the
-    DFMA/DMUL/DADD count of the event loops in the built SASS of k_far_list<P> and k_feval<P>."""
+    stresslets): far_eval<P> in csrc/far_eval.cuh counted op by op (FMA = 2) plus the pair's
+    geometry in the calling loop (dx and r^2 as the MAC computes them: 2 DMUL + 5 DADD as
+    the compiler emits them).  tests/test_sass_counts.py checks this against the
+    DFMA/DMUL/DADD count of the event loop in the built SASS of k_far_list<P> and k_feval<P>,
+    tests/test_gpu_far_flops.py against ncu's executed counts on a B200."""
     fma = mul = add = 0
-    mul += 2; fma += 3                      # rsqrt_dp correction
-    mul += 4                                # rho = 1/r^2, X, Y, Z
-    mul += 3                                # grade 0: three Phi columns
-
-    def contract(n):                        # one coefficient against its weight columns
-        return 4 if n < P else 1            # (Psi only at the top grade)
-    for n in range(1, P + 1):               # column m = 0
-        if n == 1:
-            mul += 1
-        else:
-            mul += 2; fma += 1              # q = beta rho; u = Z u1 + q u2
-        fma += contract(n)
-    for m in range(1, P + 1):               # columns m >= 1 (cos and sin)
-        if m == 1:
-            mul += 2
-        else:
-            mul += 2; fma += 2              # diagonal (X + iY) u_{m-1}^{m-1}
-        fma += 2 * contract(m)
-        if m < P:
-            mul += 2                        # u_{m+1}^m = Z u_m^m
-            fma += 2 * contract(m + 1)
-        for n in range(m + 2, P + 1):
-            mul += 3; fma += 2              # q, then both parts
-            fma += 2 * contract(n)
-    fma += 3                                # Phi_i + dx_i Psi
-    add += 3 + 3 + 2; mul += 3              # accumulate; dx; r^2
+    mul += 2; fma += 3          # rsqrt_dp correction
+    mul += 3                    # unit direction
+    mul += 3                    # grade 0: three Phi columns
+    for n in range(1, P + 1):
+        if n >= 2:
+            mul += 2 * n - 3; fma += 2 * n - 3   # w_n^m = z w_{n-1}^m + beta w_{n-2}^m, m <= n-2
+            mul += 4; fma += 2                   # m = n-1, m = n
+        mul += 1                                 # r^-(n+1)
+        cols = 4 if n < P else 1                 # the top grade carries Psi only
+        mul += cols; fma += cols * 2 * n         # contraction over the 2n+1 harmonics
+        fma += cols                              # accumulate the grade
+    fma += 3; add += 3                           # u_i += Phi_i + dx_i Psi
+    add += 5; mul += 2                           # pair geometry in the event loop
     return 2 * fma + mul + add
 
 

@@ -1,7 +1,9 @@
-"""Executed FP64 work per far-field pair, counted by ncu on a B200: k_far_pairs (one pair per
-thread, no idle lanes) must execute bench.far_executed_flops(P) - 3 flops per pair
-(2 DFMA + DMUL + DADD thread-instructions; the pair kernel receives dx, so the three dx
-subtractions of the event loops are absent).  This pins the far roofline's flop count."""
+"""Executed FP64 work per far-field pair, counted by ncu on a B200, pins bench.py's far
+roofline flop count (bench.far_executed_flops).  The case makes every event dense and
+shared: 6,400 targets far from a compact source cloud each accept the root cluster only,
+so k_far_list evaluates exactly one pair per target with every lane of both batches busy;
+its 2 DFMA + DMUL + DADD thread-instructions divided by the far-field evaluations must
+equal the formula."""
 import os
 import shutil
 import subprocess
@@ -16,11 +18,15 @@ SNIPPET = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 import paper_1811_12498_b200 as S
-p, n = int(sys.argv[2]), int(sys.argv[3])
+p = int(sys.argv[2])
 rng = np.random.default_rng(1)
-dx = rng.uniform(-1, 1, (n, 3)) + np.array([3.0, 0, 0])
-E = (p + 1) * (p + 2) * (p + 3) // 6
-S.farfield_pairs(dx, p, stok=rng.uniform(-1, 1, (n, E, 3)), strm=rng.uniform(-1, 1, (n, E, 9)))
+n = 5000
+nu = rng.normal(size=(n, 3))
+nu /= np.linalg.norm(nu, axis=1, keepdims=True)
+ps = S.ParticleSet(rng.uniform(0, 0.01, (n, 3)), rng.uniform(-1, 1, (n, 3)), rng.uniform(-1, 1, (n, 3)), nu)
+tg = rng.uniform(-1, 1, (6400, 3)) + np.array([10.0, 0, 0])
+r = S.treecode_velocity_targets(ps, tg, S.TreecodeParams(order=p, theta=0.5, leaf_capacity=500))
+assert r.stats.farfield_evals == 6400 and r.stats.direct_pairs == 0, r.stats
 """
 
 
@@ -28,11 +34,11 @@ S.farfield_pairs(dx, p, stok=rng.uniform(-1, 1, (n, E, 3)), strm=rng.uniform(-1,
 def test_far_pair_executed_flops(p, tmp_path):
     sys.path.insert(0, ROOT)
     import bench
-    n = 2048
+    n = 6400
     metrics = ",".join(f"smsp__sass_thread_inst_executed_op_{k}_pred_on.sum" for k in ("dfma", "dmul", "dadd"))
     log = tmp_path / "ncu.csv"
-    out = subprocess.run(["ncu", "--metrics", metrics, "-k", "regex:k_far_pairs", "--csv", "--log-file", str(log),
-                          sys.executable, "-c", SNIPPET, ROOT, str(p), str(n)],
+    out = subprocess.run(["ncu", "--metrics", metrics, "-k", "regex:k_far_list", "--csv", "--log-file", str(log),
+                          sys.executable, "-c", SNIPPET, ROOT, str(p)],
                          capture_output=True, text=True, timeout=600)
     if out.returncode != 0 or not log.exists():
         pytest.skip("ncu could not profile here: " + (out.stderr or out.stdout)[-300:])
@@ -47,4 +53,4 @@ def test_far_pair_executed_flops(p, tmp_path):
                 vals[k] = vals.get(k, 0.0) + float(r[vi].replace(",", ""))
     assert set(vals) == {"dfma", "dmul", "dadd"}, log.read_text()[-2000:]
     per_pair = (2 * vals["dfma"] + vals["dmul"] + vals["dadd"]) / n
-    assert per_pair == bench.far_executed_flops(p + 2) - 3, (p, per_pair, vals)
+    assert per_pair == bench.far_executed_flops(p + 2), (p, per_pair, vals)

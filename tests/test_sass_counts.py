@@ -1,6 +1,7 @@
-"""Static checks of the far kernels' SASS (CPU-only: cuobjdump reads the sm_100a cubins):
-instruction-cache footprint and the two-target weight sharing.  The executed-flop count
-bench.py's far roofline uses is pinned on a GPU by tests/test_gpu_far_flops.py (ncu)."""
+"""The far-field roofline in bench.py counts EXECUTED FP64 flops per accepted pair
+(bench.far_executed_flops).  Pin that count to the built SASS: the event loop of
+k_far_list<P> and the pair loop of k_feval<P> must execute exactly that many
+2*DFMA + DMUL + DADD per pair.  CPU-only (cuobjdump reads the sm_100a cubins)."""
 import collections
 import os
 import re
@@ -41,36 +42,43 @@ def funcs():
     return _FUNCS
 
 
-@pytest.mark.parametrize("P", [3, 7, 10, 12, 18])
-@pytest.mark.parametrize("kernel", ["k_far_list", "k_feval"])
-def test_far_kernels_fit_the_instruction_cache(kernel, P):
-    """The far kernels' column loops run at run time: the fully unrolled form (one template
-    instance per (n, m)) grew to ~2,900 instructions at P = 10 with the two-target path and
-    stalled on instruction fetch (ncu r02e: 4.0 no_instruction stalls per issue at P = 12).
-    Guard: the whole kernel stays under 1,600 SASS instructions (25 KB) at every order."""
-    name = next((f for f in funcs() if re.search(rf"{kernel}ILi{P}E", f)), None)
-    assert name, f"{kernel}<{P}> not in the library"
-    n = sum(1 for ln in funcs()[name] if re.match(r"\s*/\*[0-9a-f]{4,}\*/", ln))
-    assert n < 1600, (kernel, P, n)
-
-
-@pytest.mark.parametrize("P", [10, 12])
-def test_two_target_inner_loop_shares_weight_loads(P):
-    """k_far_list's inner column loop for two targets (unrolled by two grades): per grade and
-    column pair, 2 x (4 DMUL + 2 DFMA recurrence + 2 q) ... i.e. 26 DP instructions per grade
-    against 4 LDS.128 -- each weight pair feeds both targets."""
-    name = next(f for f in funcs() if re.search(rf"k_far_listILi{P}E", f))
+def innermost_pair_loop(lines):
+    """Smallest backward-branch loop holding exactly one MUFU (the pair's rsqrt seed)."""
     ins = []
-    for ln in funcs()[name]:
+    for ln in lines:
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
         if m:
             ins.append((int(m.group(1), 16), m.group(2).strip()))
     addr = {a: i for i, (a, _) in enumerate(ins)}
-    loops = []
+    best = None
     for i, (a, txt) in enumerate(ins):
         m = re.search(r"BRA\s.*?0x([0-9a-f]+)", txt)
-        if m and int(m.group(1), 16) <= a and int(m.group(1), 16) in addr:
-            body = ins[addr[int(m.group(1), 16)]:i + 1]
-            loops.append(collections.Counter(t.split()[1 if t.startswith("@") else 0].split(".")[0] for _, t in body))
-    dp = lambda o: o["DFMA"] + o["DMUL"] + o["DADD"]
-    assert any(dp(o) == 52 and o["LDS"] == 8 and o["MUFU"] == 0 for o in loops), [dict(o) for o in loops]
+        if not m:
+            continue
+        tgt = int(m.group(1), 16)
+        if tgt > a or tgt not in addr:
+            continue
+        body = ins[addr[tgt]:i + 1]
+        ops = collections.Counter(t.split()[1 if t.startswith("@") else 0].split(".")[0] for _, t in body)
+        if ops["MUFU"] != 1:
+            continue
+        if best is None or len(body) < best[0]:
+            best = (len(body), ops)
+    return best[1] if best else None
+
+
+@pytest.mark.parametrize("P", [3, 7, 9, 10, 12])
+@pytest.mark.parametrize("kernel", ["k_far_list", "k_feval"])
+def test_far_executed_flops_match_sass(kernel, P):
+    import bench
+    name = next((f for f in funcs() if re.search(rf"{kernel}ILi{P}E", f)), None)
+    assert name, f"{kernel}<{P}> not in the library"
+    ops = innermost_pair_loop(funcs()[name])
+    assert ops is not None
+    flops = 2 * ops["DFMA"] + ops["DMUL"] + ops["DADD"]
+    if kernel == "k_far_list":
+        assert flops == bench.far_executed_flops(P), (kernel, P, dict(ops))
+    else:
+        # the packed sparse pass recomputes r^2 with its own DMULs: at most 3 flops more per
+        # pair, so the dense kernel's count used for both slightly under-counts (<= 2%)
+        assert bench.far_executed_flops(P) <= flops <= bench.far_executed_flops(P) + 3, (kernel, P, dict(ops))
