@@ -117,3 +117,95 @@ def test_debug_build_mac_containment_check(S, tmp_path):
         assert out.returncode == 0, out.stderr
         res[tag] = np.load(f)
     assert res["debug"].tobytes() == res["release"].tobytes()
+
+
+def _dict(ps):
+    return dict(position=ps.position, force_weight=ps.force_weight, dipole_weight=ps.dipole_weight,
+                normal=ps.normal)
+
+
+def test_signed_zero_extremes_pinned(S, need_ref):
+    """the device's order-free min/max puts -0.0 below +0.0, where the
+    reference's tight_box keeps the first-seen of two equal extremes.  Pinned: the trees are
+    identical except possibly in the sign of a zero bound (centre / bbox), and the
+    velocities agree to 1e-12 (a signed zero never changes a distance)."""
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0.0, 1.0, (400, 3))
+    pos[0] = [0.0, 0.3, 0.7]
+    pos[1] = [-0.0, 0.6, 0.2]   # both signed zeros are the x extreme of the root
+    pos[2] = [0.5, -0.0, 0.4]
+    pos[3] = [0.2, 0.0, 0.9]    # and of y, in the other order
+    f = rng.uniform(-1, 1, (400, 3))
+    ps = S.ParticleSet(pos, f)
+    sel = S.KernelSelection.stokeslet_only()
+    for n0 in (1, 16, 500):
+        T = S.build_tree(ps, n0, True)
+        R = need_ref.RefContext(dict(position=pos, force_weight=f), 0, 0.5, n0, True, sto=True, stre=False).tree()
+        assert np.array_equal(T.to_original, R.to_original)
+        assert np.array_equal(T.begin, R.begin) and np.array_equal(T.end, R.end)
+        assert np.array_equal(T.children, R.children)
+        same_up_to_zero_sign = (T.geom == R.geom)  # -0.0 == +0.0 numerically
+        assert same_up_to_zero_sign.all()
+        differ = T.geom.view(np.uint64) != R.geom.view(np.uint64)
+        assert np.all(T.geom[differ] == 0.0)  # only zero signs may differ
+        prm = S.TreecodeParams(order=4, theta=0.5, leaf_capacity=n0, kernels=sel)
+        u = S.treecode_velocity(ps, prm).velocity
+        u_ref, _, _ = need_ref.ref_parallel_velocity(dict(position=pos, force_weight=f), 4, 0.5, n0, True,
+                                                     sto=True, stre=False)
+        assert S.relative_error(u_ref, u) <= 1e-12
+
+
+def test_subnormal_distance_pinned(S, need_ref):
+    """the near field tests the coincident-pair condition once per entry
+    (its sums turn NaN), so a pair whose r^2 underflows to a subnormal raises domain_error on
+    the device; the reference (which only tests r^2 == 0) returns inf / NaN velocities.
+    Pinned on both sides."""
+    rng = np.random.default_rng(4)
+    pos = rng.uniform(0.0, 1.0, (50, 3))
+    pos[3] = [0.0, 0.25, 0.75]
+    pos[7] = [1e-160, 0.25, 0.75]  # r^2 = 1e-320: subnormal, not zero
+    f = rng.uniform(-1, 1, (50, 3))
+    ps = S.ParticleSet(pos, f)
+    prm = S.TreecodeParams(order=3, theta=0.5, leaf_capacity=1000, kernels=S.KernelSelection.stokeslet_only())
+    u_ref, _, _ = need_ref.ref_parallel_velocity(dict(position=pos, force_weight=f), 3, 0.5, 1000, True,
+                                                 sto=True, stre=False)
+    assert not np.isfinite(u_ref[[3, 7]]).all() and np.isfinite(np.delete(u_ref, [3, 7], axis=0)).all()
+    with pytest.raises(S.DomainError):
+        S.treecode_velocity(ps, prm)
+
+
+OVERFLOW_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+rng = np.random.default_rng(4)
+pos = rng.uniform(0.0, 1.0, (50, 3)); pos[7] = [1e155, 0.0, 0.0]   # |d|^2 = inf for every pair with it
+f = rng.uniform(-1, 1, (50, 3))
+if sys.argv[2] == "ref":
+    from oracle import oracle as O
+    O.ref_parallel_velocity(dict(position=pos, force_weight=f), 3, 0.5, 1000, True, sto=True, stre=False)
+else:
+    import paper_1811_12498_b200 as S
+    S.treecode_velocity(S.ParticleSet(pos, f), S.TreecodeParams(order=3, theta=0.5, leaf_capacity=1000,
+                                                                 kernels=S.KernelSelection.stokeslet_only()))
+print("completed")
+"""
+
+
+def test_overflowing_distance_trips_the_mac_assert(S, need_ref):
+    """|coordinates| ~ 1e155 make |d|^2 = inf, so the MAC (r_c^2 <= theta^2 |d|^2) accepts
+    the root cluster, which holds the target: the reference's own assert (engine.hpp:88-89)
+    aborts, and this library's debug build (ST_DEBUG_CHECKS) fails the call with the same
+    message.  The release build does not check (the reference built with NDEBUG neither)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ref = subprocess.run([sys.executable, "-c", OVERFLOW_SCRIPT, root, "ref"], capture_output=True, text=True,
+                         timeout=300)
+    assert ref.returncode != 0 and "MAC accepted a cluster containing the target" in ref.stderr
+    dbg = os.path.join(root, "paper_1811_12498_b200", "libstokestree_b200_debug.so")
+    if not os.path.exists(dbg):
+        pytest.skip("debug library not built")
+    out = subprocess.run([sys.executable, "-c", OVERFLOW_SCRIPT, root, "gpu"], capture_output=True, text=True,
+                         timeout=300, env=dict(os.environ, ST_LIB_PATH=dbg))
+    assert out.returncode != 0 and "MAC accepted a cluster containing the target" in out.stderr, out.stderr
