@@ -362,7 +362,10 @@ def run_reference(args, cfg):
 def config_block(cfg, args, world):
     par = "one GPU"
     if world > 1:
-        par = (f"targets sharded over {world} GPUs by work-balanced Morton batches, tree+moments replicated"
+        split = args.gather == "peer" and args.moments == "split"
+        par = (f"targets sharded over {world} GPUs by work-balanced Morton batches, tree replicated, "
+               + ("moment pass split by subtrees with the weight rows exchanged over NCCL" if split
+                  else "moments replicated")
                + (", shards stored into rank 0's output by the epilogue kernel (CUDA IPC, NVLink)"
                   if args.gather == "peer" else ", batch-order slices all-gathered over NCCL"))
     return {"workload": cfg["desc"], "n_sources": cfg["n"], "n_targets": cfg["targets"] or cfg["n"],
@@ -464,6 +467,8 @@ def run_gpu(args, cfg):
         dist.broadcast_object_list(obj, 0)
         peer_out = dout.data_ptr() if rank == 0 else S.ipc_open(*obj[0])
         done = torch.zeros(1, dtype=torch.float32, device=dev)
+        from paper_1811_12498_b200.distributed import collective_exchange
+        exchange = collective_exchange(dist, local)
     elif world > 1:
         dbatch = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
         torig = torch.empty(nt, dtype=torch.int32, device=dev)
@@ -475,8 +480,14 @@ def run_gpu(args, cfg):
             return S.treecode_velocity_device(*ptrs, n, prm, dout.data_ptr(), targets_ptr=tp, n_targets=ntp,
                                               stream=sptr)
         if peer_out is not None:
-            r = S.treecode_velocity_device(*ptrs, n, prm, peer_out, targets_ptr=tp, n_targets=ntp, shard=rank,
-                                           n_shards=world, stream=sptr)
+            if args.moments == "split":
+                # each rank computes its subtrees' moments; the weight rows are exchanged by
+                # one broadcast per rank on the call's stream (NCCL over NVLink)
+                r = S.treecode_velocity_device_split(*ptrs, n, prm, peer_out, exchange, targets_ptr=tp, n_targets=ntp,
+                                                     shard=rank, n_shards=world, stream=sptr)
+            else:
+                r = S.treecode_velocity_device(*ptrs, n, prm, peer_out, targets_ptr=tp, n_targets=ntp, shard=rank,
+                                               n_shards=world, stream=sptr)
             dist.all_reduce(done)  # every shard's stores into rank 0's buffer have completed
             return r
         # every rank: same tree/moments, its work-balanced slice of the Morton-ordered batches in
@@ -806,6 +817,9 @@ def main():
     ap.add_argument("--ref-full-max", type=int, default=1_000_000,
                     help="reference arm: run the whole workload when N <= this (cfg0, cfg1), else sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--moments", default="split", choices=["split", "replicated"],
+                    help="N>1: each rank computes its share of the moment pass and the ranks exchange the weight "
+                         "rows (split), or every rank computes all of it (replicated)")
     ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
                     help="N>1: shards stored into rank 0's buffer by the epilogue kernel over CUDA IPC "
                          "(peer), or batch-order slices all-gathered over NCCL and scattered (nccl)")

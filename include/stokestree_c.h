@@ -161,6 +161,34 @@ st_status st_interaction_lists(const st_particles* src, const st_params* params,
                                size_t cap, int32_t* far, int32_t* near, int64_t* n_far,
                                int64_t* n_near);
 
+/* ---- one process per GPU, moment pass split over the ranks ----
+ * As st_treecode_velocity_device(shard, n_shards), but the moment pass is not replicated:
+ * each rank computes the moments and far-field weights of its share of the tree (whole
+ * subtrees, balanced by particle count), and the ranks exchange them through `exchange`,
+ * which the library calls once per call (on every rank, also a rank with no targets),
+ * after the rank's own rows are queued on `ex->stream` and before any far-field kernel.
+ * The callback must make every rank's rows of ex->w and units of ex->m present in this
+ * rank's buffers in stream order on ex->stream -- e.g. one NCCL broadcast per rank of
+ * rows [w_cuts[r], w_cuts[r+1]) and units [m_cuts[r], m_cuts[r+1]) -- and return 0
+ * (non-zero fails the call with ST_RUNTIME_ERROR).  The cut points are identical on every
+ * rank.  The velocities are bit-identical to the replicated path's.  exchange == NULL or
+ * n_shards == 1: the replicated path.  (DESIGN.md section 6.) */
+typedef struct st_shard_exchange {
+    int shard, n_shards;
+    double* w;             /* device: folded far-field weights, ncl rows of w_row doubles   */
+    size_t w_row, ncl;
+    const size_t* w_cuts;  /* host, n_shards + 1: rank r produced rows [w_cuts[r], w_cuts[r+1]) */
+    double* m;             /* device: moments of the n_units subtree roots, m_row doubles each */
+    size_t m_row, n_units;
+    const size_t* m_cuts;  /* host, n_shards + 1: rank r produced units [m_cuts[r], m_cuts[r+1]) */
+    void* stream;          /* the call's stream (cudaStream_t): enqueue the exchange on it    */
+} st_shard_exchange;
+typedef int (*st_exchange_fn)(void* ctx, const st_shard_exchange* ex);
+st_status st_treecode_velocity_device_split(const st_particles* src_device, const double* targets_device,
+                                            size_t n_targets, const st_params* params, double* u_out_device,
+                                            int shard, int n_shards, void* stream, st_exchange_fn exchange,
+                                            void* ctx, st_stats* stats);
+
 /* Shard evaluation for collective gathers (one rank per GPU): like
  * st_treecode_velocity_device but the shard's velocities are written in BATCH order
  * (Morton order of 32-target batches) into u_batch[3*t0 .. 3*t1), so every rank owns a

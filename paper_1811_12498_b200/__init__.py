@@ -47,7 +47,8 @@ __all__ = [
     "farfield_pairs", "taylor_coeffs", "relative_error", "interaction_lists", "generate", "shard_cuts", "fp64_peak", "device_count",
     "mi_count", "lib_path", "load_library", "EXPORTED_SYMBOLS", "sphere_particles", "cube_particles",
     "write_particles", "read_particles", "treecode_velocity_sweep",
-    "ipc_export", "ipc_open", "ipc_close", "release_workspace",
+    "ipc_export", "ipc_open", "ipc_close", "release_workspace", "treecode_velocity_device_split",
+    "ShardExchange",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -66,6 +67,7 @@ EXPORTED_SYMBOLS = (
     "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
     "st_read_particles", "st_loaded_copy", "st_loaded_free", "st_treecode_shard_device", "st_unbatch_device",
     "st_taylor_coeffs", "st_ipc_export", "st_ipc_open", "st_ipc_close", "st_release_workspace",
+    "st_treecode_velocity_device_split",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -105,6 +107,19 @@ class _Stats(C.Structure):
                 ("time_near_s", C.c_double), ("time_h2d_s", C.c_double),
                 ("time_d2h_s", C.c_double), ("gpu_launches", C.c_uint64)]
 
+
+class ShardExchange(C.Structure):
+    """st_shard_exchange (stokestree_c.h): the split moment pass's buffers on this rank."""
+    _fields_ = [("shard", C.c_int), ("n_shards", C.c_int), ("w", C.c_void_p), ("w_row", C.c_size_t),
+                ("ncl", C.c_size_t), ("w_cuts", C.POINTER(C.c_size_t)), ("m", C.c_void_p), ("m_row", C.c_size_t),
+                ("n_units", C.c_size_t), ("m_cuts", C.POINTER(C.c_size_t)), ("stream", C.c_void_p)]
+
+    def cuts(self, which):
+        p = self.w_cuts if which == "w" else self.m_cuts
+        return [int(p[i]) for i in range(self.n_shards + 1)]
+
+
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(ShardExchange))
 
 _lib = None
 
@@ -166,6 +181,8 @@ def load_library():
     L.st_loaded_free.argtypes = [vp]
     L.st_loaded_free.restype = None
     L.st_release_workspace.argtypes = []
+    L.st_treecode_velocity_device_split.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, i, vp, EXCHANGE_FN,
+                                                    vp, P(_Stats)]
     for name in EXPORTED_SYMBOLS:
         if name not in ("st_abi_version", "st_last_error", "st_tree_num_clusters",
                         "st_tree_num_particles", "st_tree_free", "st_sphere_count", "st_loaded_free"):
@@ -409,6 +426,37 @@ def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole
     st = _Stats()
     _check(L.st_treecode_velocity_device_ev(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr,
                                             shard, n_shards, stream, weights_event or None, C.byref(st)))
+    return _result(None, st)
+
+
+def treecode_velocity_device_split(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],
+                                   normal_ptr: Optional[int], n: int, params: TreecodeParams, u_out_ptr: int,
+                                   exchange, targets_ptr: Optional[int] = None, n_targets: int = 0, shard: int = 0,
+                                   n_shards: int = 1, stream: int = 0) -> VelocityResult:
+    """Device-resident shard call with the moment pass split over the ranks
+    (st_treecode_velocity_device_split).  ``exchange(ex: ShardExchange) -> None`` is called
+    once, on the call's stream, to move every rank's weight rows and unit moments into this
+    rank's buffers (e.g. NCCL broadcasts); an exception in it fails the call."""
+    L = load_library()
+    cp = _Particles(n, position_ptr, force_ptr, dipole_ptr, normal_ptr)
+    prm = params._c()
+    st = _Stats()
+    err = []
+
+    def cb(_ctx, exp):
+        try:
+            exchange(exp.contents)
+            return 0
+        except BaseException as e:  # reported through the call's status
+            err.append(e)
+            return 1
+
+    fn = EXCHANGE_FN(cb)
+    code = L.st_treecode_velocity_device_split(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr, shard,
+                                               n_shards, stream, fn, None, C.byref(st))
+    if err:
+        raise err[0]
+    _check(code)
     return _result(None, st)
 
 

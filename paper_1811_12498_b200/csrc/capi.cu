@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <map>
 #include <cmath>
 #include <cstring>
@@ -360,8 +361,6 @@ int far_sparse_max() {
     return v;
 }
 
-void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
-
 struct ShardOut {
     int w0 = 0, w1 = 0;         // warp (32-target batch) range evaluated
     DevArray<uint32_t> torig;   // batch position -> original target index (if requested)
@@ -376,10 +375,17 @@ bool moments_inline() {
 // `weights_ready` (if set) is waited for after the tree build, which needs positions only.
 // Validation runs on the device after that wait and is read back with the results;
 // callers raise in the reference's order with raise_flags().
+// exchange (if set and nshards > 1): the moment pass is split over the ranks
+// (moments.cuh MomentsSplit); the callback moves the rows between them before the far field.
+struct SplitExchange {
+    st_exchange_fn fn = nullptr;
+    void* ctx = nullptr;
+};
+
 void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in, const st_params& prm,
                   double* d_out, uint64_t* d_per_target, int shard, int nshards, cudaStream_t s,
                   RunOut& ro, bool out_batch = false, ShardOut* so = nullptr,
-                  cudaEvent_t weights_ready = nullptr) {
+                  cudaEvent_t weights_ready = nullptr, const SplitExchange* xchg = nullptr) {
     const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
     const size_t n = src.n;
     const bool same = d_targets == nullptr;
@@ -428,13 +434,68 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     Event em;
     em.record(aux.s);
     DevArray<double> M, W;
-    compute_moments_device(tree, rec.get(), prm.order, sto, str, aux.s, M, &mplan);
-    fold_weights_device(M.get(), tree.ncl, prm.order, sto, str, aux.s, W);
-    M.reset();
+    const bool split = xchg && xchg->fn && nshards > 1;
+    const int Pw = prm.order + (str ? 2 : 1);
+    const size_t w_row = (size_t)4 * (Pw + 1) * (Pw + 1), m_row = (size_t)12 * mi_count(prm.order);
+    MomentsSplit sp;
+    DevArray<double> Mu;                   // moments of the split's subtree roots, packed
+    DevArray<int32_t> d_units, d_top;      // unit roots, top clusters (device lists)
+    if (!split) {
+        compute_moments_device(tree, rec.get(), prm.order, sto, str, aux.s, M, &mplan);
+        fold_weights_device(M.get(), tree.ncl, prm.order, sto, str, aux.s, W);
+        M.reset();
+    } else {
+        // this rank's subtrees only: leaves, M2M up to depth L, their weights and roots
+        sp = split_moments(mplan, tree.ncl, nshards);
+        const MomentsPlan own = shard_moments_plan(mplan, sp, shard);
+        compute_moments_device(tree, rec.get(), prm.order, sto, str, aux.s, M, &own);
+        W.alloc((size_t)tree.ncl * w_row, aux.s);
+        const size_t u0 = sp.unit_cuts[shard], u1 = sp.unit_cuts[shard + 1];
+        std::vector<int32_t> rows;
+        if (u0 < u1) {
+            const int lo = sp.units[u0], hi = mplan.info[sp.units[u1 - 1]].z;
+            for (int v = lo; v < hi; ++v)
+                if (!(mplan.depth[v] < sp.depth && !mplan.info[v].w)) rows.push_back(v);
+        }
+        DevArray<int32_t> d_rows(rows.size(), aux.s);
+        if (!rows.empty())
+            ST_CUDA(cudaMemcpyAsync(d_rows.get(), rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, aux.s));
+        fold_weights_rows_device(M.get(), d_rows.get(), (int)rows.size(), prm.order, sto, str, aux.s, W.get());
+        d_units.alloc(sp.units.size(), aux.s);
+        ST_CUDA(cudaMemcpyAsync(d_units.get(), sp.units.data(), sp.units.size() * 4, cudaMemcpyHostToDevice, aux.s));
+        Mu.alloc(sp.units.size() * m_row, aux.s);
+        gather_rows_device(M.get(), d_units.get() + u0, (int)(u1 - u0), m_row, Mu.get() + u0 * m_row, false, aux.s);
+        d_top.alloc(sp.top_ids.size(), aux.s);
+        if (!sp.top_ids.empty())
+            ST_CUDA(cudaMemcpyAsync(d_top.get(), sp.top_ids.data(), sp.top_ids.size() * 4, cudaMemcpyHostToDevice,
+                                    aux.s));
+    }
     e2.record(aux.s);
     // ST_MOMENTS_INLINE=1 (measurement only): nothing overlaps the moment pass, so
     // time_moments_s is its own duration (bench.py's moments roofline)
     if (moments_inline()) ST_CUDA(cudaStreamWaitEvent(s, e2.e, 0));
+    // split: after this rank's rows exist, the exchange, then every rank shifts and folds
+    // the top levels itself; queued on s before the first far kernel (launch_eval)
+    std::function<void()> complete_weights = [&] {
+        ST_CUDA(cudaStreamWaitEvent(s, e2.e, 0));
+        st_shard_exchange ex;
+        ex.shard = shard;
+        ex.n_shards = nshards;
+        ex.w = W.get();
+        ex.w_row = w_row;
+        ex.ncl = (size_t)tree.ncl;
+        ex.w_cuts = sp.w_cuts.data();
+        ex.m = Mu.get();
+        ex.m_row = m_row;
+        ex.n_units = sp.units.size();
+        ex.m_cuts = sp.unit_cuts.data();
+        ex.stream = s;
+        if (xchg->fn(xchg->ctx, &ex) != 0) fail(ST_RUNTIME_ERROR, "shard exchange callback failed");
+        gather_rows_device(Mu.get(), d_units.get(), (int)sp.units.size(), m_row, M.get(), true, s);
+        const MomentsPlan top = top_moments_plan(sp);
+        compute_moments_device(tree, rec.get(), prm.order, sto, str, s, M, &top, true);
+        fold_weights_rows_device(M.get(), d_top.get(), (int)sp.top_ids.size(), prm.order, sto, str, s, W.get());
+    };
 
     // batch order of the targets: 63-bit Morton order in their tight box (one radix sort,
     // done on the second stream above)
@@ -506,7 +567,7 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     fo.out = d_out;
     EvalTimes tm;
     tm.origin = e0.e;
-    launch_eval(sto, str, a, &fo, 1, s, &tm, e2.e);
+    launch_eval(sto, str, a, &fo, 1, s, &tm, e2.e, split ? &complete_weights : nullptr);
     e3.record(s);
 
     ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -547,7 +608,7 @@ void fill_stats(st_stats* st, const RunOut& ro) {
     st->time_near_s = ro.t_near;
 }
 
-void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts) {
+void shard_cuts_impl(size_t n, const double* w, int k, size_t* cuts) {
     double total = 0.0;
     for (size_t i = 0; i < n; ++i) total += w[i] > 0 ? w[i] : 0.0;
     cuts[0] = 0;
@@ -664,6 +725,67 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     ro.t_total = secs(e0, e3);
 }
 
+// In-process exchange of the split moment pass (multi_device): every device thread
+// publishes its rows, waits for the others (a host barrier), pulls the other devices'
+// rows over NVLink (cudaMemcpyPeerAsync after the owner's event), and waits again before
+// any owner may free its buffers.  A thread that fails breaks the barrier for the others.
+struct PeerGroup {
+    int D = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0, gen = 0;
+    bool broken = false;
+    std::vector<st_shard_exchange> ex;
+    std::vector<int> dev;
+    std::vector<cudaEvent_t> ready;
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (broken) fail(ST_RUNTIME_ERROR, "devices: another device failed");
+        const int g = gen;
+        if (++arrived == D) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g || broken; });
+            if (broken) fail(ST_RUNTIME_ERROR, "devices: another device failed");
+        }
+    }
+    void fail_all() {
+        std::lock_guard<std::mutex> lk(mu);
+        broken = true;
+        cv.notify_all();
+    }
+};
+struct PeerCtx {
+    PeerGroup* g;
+    int d;
+};
+
+int peer_exchange(void* vctx, const st_shard_exchange* ex) {
+    PeerCtx* c = static_cast<PeerCtx*>(vctx);
+    PeerGroup& g = *c->g;
+    cudaStream_t s = static_cast<cudaStream_t>(ex->stream);
+    ST_CUDA(cudaEventRecord(g.ready[c->d], s));
+    g.ex[c->d] = *ex;
+    g.wait();  // every device's rows are queued and its event recorded
+    for (int q = 0; q < g.D; ++q) {
+        if (q == c->d) continue;
+        const st_shard_exchange& o = g.ex[q];
+        ST_CUDA(cudaStreamWaitEvent(s, g.ready[q], 0));
+        const size_t r0 = o.w_cuts[q], r1 = o.w_cuts[q + 1], u0 = o.m_cuts[q], u1 = o.m_cuts[q + 1];
+        if (r1 > r0)
+            ST_CUDA(cudaMemcpyPeerAsync(ex->w + r0 * ex->w_row, g.dev[c->d], o.w + r0 * o.w_row, g.dev[q],
+                                        (r1 - r0) * o.w_row * sizeof(double), s));
+        if (u1 > u0)
+            ST_CUDA(cudaMemcpyPeerAsync(ex->m + u0 * ex->m_row, g.dev[c->d], o.m + u0 * o.m_row, g.dev[q],
+                                        (u1 - u0) * o.m_row * sizeof(double), s));
+    }
+    ST_CUDA(cudaStreamSynchronize(s));
+    g.wait();  // nobody reads another device's buffers any more
+    return 0;
+}
+
 // Replicated-data multi-GPU in one process (PAPER.md:986-1030 with GPUs for MPI ranks):
 // one host thread per logical device uploads the inputs, rebuilds the (bit-identical)
 // tree and moments and evaluates its work-balanced shard of the Morton-ordered batches.
@@ -692,6 +814,18 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
         cudaGetLastError();
         pool_grant_peer(dev0, dev);  // the output buffers below come from device 0's pool
     }
+    // the split moment pass copies weight rows between every pair of devices
+    for (int a = 0; a < std::min(D, ndev); ++a)
+        for (int b = 0; b < std::min(D, ndev); ++b) {
+            const int da = (dev0 + a) % ndev, db = (dev0 + b) % ndev;
+            int can = 0;
+            if (da == db || cudaDeviceCanAccessPeer(&can, db, da) != cudaSuccess || !can) continue;
+            ST_CUDA(cudaSetDevice(db));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(da, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+            pool_grant_peer(da, db);
+        }
     ST_CUDA(cudaSetDevice(dev0));
     OwnedStream os0;
     cudaStream_t s0 = os0.s;
@@ -700,6 +834,19 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
     ST_CUDA(cudaStreamSynchronize(s0));  // allocations complete before other devices store into them
     std::vector<RunOut> ros(D);
     std::vector<std::exception_ptr> errs(D);
+    // the moment pass split over the devices, rows exchanged device to device (peer_exchange)
+    PeerGroup grp;
+    grp.D = D;
+    grp.ex.resize(D);
+    grp.dev.resize(D);
+    grp.ready.assign(D, nullptr);
+    for (int d = 0; d < D; ++d) {
+        grp.dev[d] = (dev0 + d) % ndev;
+        ST_CUDA(cudaSetDevice(grp.dev[d]));
+        ST_CUDA(cudaEventCreateWithFlags(&grp.ready[d], cudaEventDisableTiming));
+    }
+    ST_CUDA(cudaSetDevice(dev0));
+    std::vector<PeerCtx> pctx(D);
     auto work = [&](int d) {
         try {
             const int dev = (dev0 + d) % ndev;
@@ -714,17 +861,26 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
                 dt.alloc(3 * nt, s);
                 h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
             }
+            pctx[d] = PeerCtx{&grp, d};
+            SplitExchange x;
+            x.fn = peer_exchange;
+            x.ctx = &pctx[d];
             run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d, D,
-                         s, ros[d]);
+                         s, ros[d], false, nullptr, nullptr, &x);
             raise_flags(ros[d]);
         } catch (...) {
             errs[d] = std::current_exception();
+            grp.fail_all();
         }
     };
     std::vector<std::thread> th;
     for (int d = 1; d < D; ++d) th.emplace_back(work, d);
     work(0);
     for (auto& t : th) t.join();  // every shard's stream has completed (run_treecode synchronises)
+    for (int d = 0; d < D; ++d) {
+        cudaSetDevice(grp.dev[d]);
+        cudaEventDestroy(grp.ready[d]);
+    }
     ST_CUDA(cudaSetDevice(dev0));
     for (auto& e : errs)
         if (e) std::rethrow_exception(e);
@@ -748,6 +904,8 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
 }
 
 }  // namespace
+
+void st::shard_cuts_host(size_t n, const double* w, int k, size_t* cuts) { shard_cuts_impl(n, w, k, cuts); }
 
 namespace st {
 st_status io_set_error(st_status s, const std::string& m) {
@@ -1038,6 +1196,36 @@ st_status st_treecode_velocity_device_ev(const st_particles* src, const double* 
         RunOut ro;
         run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro,
                      false, nullptr, static_cast<cudaEvent_t>(weights_ready));
+        raise_flags(ro);
+        fill_stats(stats, ro);
+        if (stats) stats->gpu_launches = g_launches;
+    });
+}
+
+st_status st_treecode_velocity_device_split(const st_particles* src, const double* targets, size_t n_targets,
+                                            const st_params* params, double* u_out, int shard, int n_shards,
+                                            void* stream, st_exchange_fn exchange, void* ctx, st_stats* stats) {
+    return guarded([&] {
+        g_launches = 0;
+        validate_params(params);
+        const bool sto = params->stokeslet != 0, str = params->stresslet != 0;
+        validate_shape(src, sto, str);
+        if (n_shards < 1 || shard < 0 || shard >= n_shards) fail(ST_INVALID_ARGUMENT, "shard out of range");
+        if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevParticles d;
+        d.n = src->n;
+        d.pos = src->position;
+        d.f = sto ? src->force_weight : nullptr;
+        d.h = str ? src->dipole_weight : nullptr;
+        d.nu = str ? src->normal : nullptr;
+        RunOut ro;
+        SplitExchange x;
+        x.fn = exchange;
+        x.ctx = ctx;
+        run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro,
+                     false, nullptr, nullptr, &x);
         raise_flags(ro);
         fill_stats(stats, ro);
         if (stats) stats->gpu_launches = g_launches;

@@ -303,11 +303,13 @@ __device__ __forceinline__ double fact_ratio(int q, int k) {  // q!/k! for |q-k|
 // k3 >= 2 onto the harmonic basis, write W[blk][h][4].
 template <bool STO, bool STR>
 __global__ void __launch_bounds__(kThreads)
-    k_fold(int p, int P, int Estride, const double* __restrict__ M, double* __restrict__ W) {
+    k_fold(int p, int P, int Estride, const double* __restrict__ M, double* __restrict__ W,
+           const int32_t* __restrict__ rows) {
     extern __shared__ double s_w[];  // [E(P)][4]
     const int EP = mi_count(P);
+    const size_t blk = rows ? (size_t)rows[blockIdx.x] : (size_t)blockIdx.x;
     // moments of order p are the graded prefix of any higher-order block (multi_index.hpp:110-114)
-    const double* Mb = M + (size_t)blockIdx.x * Estride * 12;
+    const double* Mb = M + blk * Estride * 12;
     const double third = 1.0 / 3.0;
 
     for (int q = threadIdx.x; q < EP; q += blockDim.x) {
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(kThreads)
     // W_hat[m] = sum_j B_s[j][m] W[j], so far_eval sums W_hat against harmonics that cost
     // two DP ops each instead of the 4-5 of the Coulomb recurrence.
     const int H = harm_count(P);
-    double* Wb = W + (size_t)blockIdx.x * H * 4;
+    double* Wb = W + blk * H * 4;
     for (int h = threadIdx.x; h < H; h += blockDim.x) {
         int s = 0;
         while ((s + 1) * (s + 1) <= h) ++s;
@@ -487,6 +489,9 @@ MomentsPlan plan_moments(const DevTree& tree, cudaStream_t s) {
     std::vector<int32_t> bylevel(ncl);
     ST_CUDA(cudaMemcpyAsync(bylevel.data(), tree.bylevel.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
+    pl.depth.assign(ncl, 0);
+    for (size_t d = 0; d + 1 < tree.level_start.size(); ++d)
+        for (int b = tree.level_start[d]; b < tree.level_start[d + 1]; ++b) pl.depth[bylevel[b]] = (int)d;
     for (int v = 0; v < ncl; ++v) {
         if (!info[v].w) continue;  // internal cluster
         const int cnt = info[v].y - info[v].x;
@@ -504,11 +509,87 @@ MomentsPlan plan_moments(const DevTree& tree, cudaStream_t s) {
             if (!info[bylevel[b]].w) ids.push_back(bylevel[b]);
         pl.lv.push_back(ids);
     }
+    pl.info = std::move(info);
+    return pl;
+}
+
+MomentsSplit split_moments(const MomentsPlan& full, int ncl, int nshards) {
+    MomentsSplit sp;
+    const std::vector<int4>& info = full.info;
+    const int maxd = (int)full.lv.size();  // internal levels; leaves may sit one deeper
+    int L = 0;
+    for (;; ++L) {
+        size_t units = 0;
+        bool deeper = false;
+        for (int v = 0; v < ncl; ++v) {
+            const int d = full.depth[v];
+            if (d == L || (d < L && info[v].w)) ++units;
+            if (d > L) deeper = true;
+        }
+        if (units >= (size_t)4 * nshards || !deeper || L > maxd) break;
+    }
+    sp.depth = L;
+    std::vector<double> wt;
+    for (int v = 0; v < ncl; ++v) {
+        const int d = full.depth[v];
+        if (d == L || (d < L && info[v].w)) {
+            sp.units.push_back(v);  // ascending v: pre-order
+            wt.push_back((double)(info[v].y - info[v].x));
+        }
+    }
+    sp.unit_cuts.assign(nshards + 1, 0);
+    shard_cuts_host(sp.units.size(), wt.data(), nshards, sp.unit_cuts.data());
+    sp.w_cuts.assign(nshards + 1, (size_t)ncl);
+    sp.w_cuts[0] = 0;
+    for (int r = 1; r < nshards; ++r)
+        sp.w_cuts[r] = sp.unit_cuts[r] < sp.units.size() ? (size_t)sp.units[sp.unit_cuts[r]] : (size_t)ncl;
+    for (int r = nshards - 1; r >= 1; --r) sp.w_cuts[r] = std::min(sp.w_cuts[r], sp.w_cuts[r + 1]);
+    sp.top.assign(std::min<size_t>(L, full.lv.size()), {});
+    for (size_t d = 0; d < sp.top.size(); ++d) {
+        sp.top[d] = full.lv[d];  // internal clusters above L
+        sp.top_ids.insert(sp.top_ids.end(), sp.top[d].begin(), sp.top[d].end());
+    }
+    return sp;
+}
+
+MomentsPlan shard_moments_plan(const MomentsPlan& full, const MomentsSplit& sp, int shard) {
+    // clusters inside this rank's units: [units[u0], next(units[u1 - 1]))
+    const size_t u0 = sp.unit_cuts[shard], u1 = sp.unit_cuts[shard + 1];
+    MomentsPlan pl;
+    pl.info = full.info;
+    pl.depth = full.depth;
+    pl.lv.assign(full.lv.size(), {});
+    if (u0 >= u1) {
+        pl.off.push_back(0);
+        return pl;
+    }
+    const int lo = sp.units[u0], hi = full.info[sp.units[u1 - 1]].z;
+    for (size_t i = 0; i < full.cl.size(); ++i) {
+        const int v = full.cl[i];
+        if (v < lo || v >= hi) continue;
+        const int nch = full.off[i + 1] - full.off[i];
+        pl.cl.push_back(v);
+        pl.off.push_back(pl.items);
+        pl.slot.push_back(nch > 1 ? pl.parts : -1);
+        if (nch > 1) pl.parts += nch;
+        pl.items += nch;
+    }
+    pl.off.push_back(pl.items);
+    for (size_t d = sp.depth; d < full.lv.size(); ++d)
+        for (int v : full.lv[d])
+            if (v >= lo && v < hi) pl.lv[d].push_back(v);
+    return pl;
+}
+
+MomentsPlan top_moments_plan(const MomentsSplit& sp) {
+    MomentsPlan pl;
+    pl.off.push_back(0);
+    pl.lv = sp.top;
     return pl;
 }
 
 void compute_moments_device(const DevTree& tree, const double* src, int p, bool sto, bool str,
-                            cudaStream_t s, DevArray<double>& M, const MomentsPlan* plan) {
+                            cudaStream_t s, DevArray<double>& M, const MomentsPlan* plan, bool keep) {
     static const bool dbg = getenv("ST_DEBUG_MOMENTS") != nullptr;
     auto stamp = [&](const char* what) {
         if (!dbg) return;
@@ -542,8 +623,10 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
             ST_CUDA(cudaMemcpyAsync(d_lvl.get(), flat.data(), sizeof(int32_t) * flat.size(), cudaMemcpyHostToDevice, s));
     }
     stamp("host lists");
-    M.alloc((size_t)ncl * E * 12, s);
-    M.zero();
+    if (!keep) {
+        M.alloc((size_t)ncl * E * 12, s);
+        M.zero();
+    }
     DevArray<double> part((size_t)std::max(parts, 1) * E * 12, s);
     stamp("alloc");
     // entries per thread (block = E/EPT rounded up to a warp): 2 (106 registers) measured
@@ -614,13 +697,47 @@ void fold_weights_device(const double* M, int nblk, int p, bool sto, bool str, c
     if (nblk == 0) return;
     auto go = [&](auto kern) {
         ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<nblk, kThreads, smem, s>>>(p, P, mi_count(pstride < 0 ? p : pstride), M, W.get());
+        kern<<<nblk, kThreads, smem, s>>>(p, P, mi_count(pstride < 0 ? p : pstride), M, W.get(), nullptr);
         ST_LAUNCH("k_fold");
         count_launch();
     };
     if (sto && str) go(k_fold<true, true>);
     else if (sto) go(k_fold<true, false>);
     else go(k_fold<false, true>);
+}
+
+void fold_weights_rows_device(const double* M, const int32_t* rows, int n, int p, bool sto, bool str,
+                              cudaStream_t s, double* W) {
+    if (n <= 0) return;
+    const int P = p + (str ? 2 : 1);
+    const size_t smem = sizeof(double) * 4 * mi_count(P);
+    auto go = [&](auto kern) {
+        ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<n, kThreads, smem, s>>>(p, P, mi_count(p), M, W, rows);
+        ST_LAUNCH("k_fold");
+        count_launch();
+    };
+    if (sto && str) go(k_fold<true, true>);
+    else if (sto) go(k_fold<true, false>);
+    else go(k_fold<false, true>);
+}
+
+__global__ void k_rows(const double* __restrict__ src, const int32_t* __restrict__ rows, int n, size_t len,
+                       double* __restrict__ dst, int scatter) {
+    const size_t i = blockIdx.y;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < len; k += (size_t)gridDim.x * blockDim.x) {
+        if (scatter) dst[(size_t)rows[i] * len + k] = src[i * len + k];
+        else dst[i * len + k] = src[(size_t)rows[i] * len + k];
+    }
+}
+
+void gather_rows_device(const double* src, const int32_t* rows, int n, size_t len, double* dst, bool scatter,
+                        cudaStream_t s) {
+    if (n <= 0 || !len) return;
+    k_rows<<<dim3((unsigned)std::min<size_t>((len + 255) / 256, 64), (unsigned)n), 256, 0, s>>>(src, rows, n, len, dst,
+                                                                                             scatter ? 1 : 0);
+    ST_LAUNCH("k_rows");
+    count_launch();
 }
 
 void export_moments_device(const double* M, int nblk, int p, bool sto, bool str, double* stok,

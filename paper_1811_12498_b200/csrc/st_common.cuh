@@ -33,6 +33,9 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define ST_CUDA(call) ::st::cuda_check((call), #call)
 #define ST_LAUNCH(what) ::st::cuda_check(cudaGetLastError(), what)
 
+// Contiguous work-balanced cut points cuts[0..k] of n units with weights w (st_shard_cuts).
+void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
+
 // Kernel-launch counter (reported as st_stats.gpu_launches).
 extern thread_local uint64_t g_launches;
 inline void count_launch(uint64_t k = 1) { g_launches += k; }

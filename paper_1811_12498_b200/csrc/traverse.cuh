@@ -1,6 +1,8 @@
 // K3-K6: MAC traversal, far field, near field, O(N^2) direct sums.
 #pragma once
 
+#include <functional>
+
 #include <vector>
 
 #include "st_common.cuh"
@@ -54,8 +56,12 @@ struct EvalTimes {
 // a.per_target.  Synchronises the stream before returning.
 // far_ready (if set): the orders' weights W are produced on another stream; the far
 // kernels wait for it (they run after the near field's evaluation).
+// before_far (if set): called once, after the first slab's near field is queued and
+// before any far kernel (also for an empty shard): the split moment pass completes W
+// there (exchange with the other ranks, top levels; capi.cu run_treecode).
 void launch_eval(bool sto, bool str, const TravArgs& a, const FarOrder* orders, int n_orders, cudaStream_t s,
-                 EvalTimes* times = nullptr, cudaEvent_t far_ready = nullptr);
+                 EvalTimes* times = nullptr, cudaEvent_t far_ready = nullptr,
+                 const std::function<void()>* before_far = nullptr);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);

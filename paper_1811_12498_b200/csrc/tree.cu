@@ -192,23 +192,34 @@ __global__ void __launch_bounds__(kTileThreads)
     k_slot_hist(uint32_t n, const double* __restrict__ pos, const uint32_t* __restrict__ perm,
                 const int32_t* __restrict__ seg_of, const double* __restrict__ seg_mid,
                 uint8_t* __restrict__ slot8, uint32_t* __restrict__ blk_cnt) {
+    // counts by warp ballots (lane k keeps the warp's count of slot k), one shared atomic
+    // per warp and slot: 8 contended shared-memory counters per element were the kernel's
+    // bottleneck
     __shared__ uint32_t cnt[8];
     if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint32_t mine = 0;
     const uint32_t base = blockIdx.x * kTile;
     for (int r = 0; r < kTile / kTileThreads; ++r) {
         const uint32_t i = base + r * kTileThreads + threadIdx.x;
-        if (i >= n) break;
-        const int s = seg_of[i];
         uint8_t slot = 8;
-        if (s >= 0) {
-            const double* p = pos + 3 * (size_t)perm[i];
-            const double* mid = seg_mid + 3 * s;
-            slot = (p[0] >= mid[0] ? 1 : 0) | (p[1] >= mid[1] ? 2 : 0) | (p[2] >= mid[2] ? 4 : 0);
-            atomicAdd(&cnt[slot], 1u);
+        if (i < n) {
+            const int s = seg_of[i];
+            if (s >= 0) {
+                const double* p = pos + 3 * (size_t)perm[i];
+                const double* mid = seg_mid + 3 * s;
+                slot = (p[0] >= mid[0] ? 1 : 0) | (p[1] >= mid[1] ? 2 : 0) | (p[2] >= mid[2] ? 4 : 0);
+            }
+            slot8[i] = slot;
         }
-        slot8[i] = slot;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const unsigned b = __ballot_sync(0xffffffffu, slot == k);
+            if (lane == k) mine += __popc(b);
+        }
     }
+    if (lane < 8 && mine) atomicAdd(&cnt[lane], mine);
     __syncthreads();
     if (threadIdx.x < 8) blk_cnt[blockIdx.x * 8 + threadIdx.x] = cnt[threadIdx.x];
 }

@@ -488,6 +488,40 @@ def test_ipc_fused_gather(world):
     assert r.returncode == 0 and "IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
+@pytest.mark.parametrize("world,case", [(2, ("cube", "30000", "6", "0.5", "300")),
+                                        (3, ("sphere", "40000", "8", "0.7", "200")),
+                                        (4, ("mixture", "30000", "5", "0.6", "100"))])
+def test_split_moment_pass_ranks(world, case):
+    """One process per rank, the moment pass split over the ranks and exchanged with
+    torch.distributed (tests/split_worker.py): bit-identical to one GPU."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(here, "split_worker.py"),
+                        *case], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "SPLIT_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("devices", [2, 3, 8])
+def test_split_moments_in_process_devices(S, devices):
+    """TreecodeParams.devices > 1 splits the moment pass over the devices and exchanges the
+    rows device to device (peer_exchange); deep trees (N0 = 20) so the split cuts below the
+    root's children.  Bit-identical to one device."""
+    for kind, n, n0, order in (("cube", 60000, 20, 6), ("sphere", 50000, 30, 10)):
+        ps = S.generate(kind, n, 9, True)
+        one = S.treecode_velocity(ps, S.TreecodeParams(order=order, theta=0.6, leaf_capacity=n0), per_target=True)
+        many = S.treecode_velocity(ps, S.TreecodeParams(order=order, theta=0.6, leaf_capacity=n0, devices=devices),
+                                   per_target=True)
+        assert many.velocity.tobytes() == one.velocity.tobytes()
+        assert np.array_equal(many.per_target, one.per_target)
+
+
 def test_pageable_and_pinned_inputs_agree(S):
     # pageable host arrays go through the pinned staging ring in 4 MB chunks (an odd size
     # here: 3 full chunks + a tail per array); pinned arrays are copied directly
