@@ -408,29 +408,36 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     DevTree tree;
     build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
     const MomentsPlan mplan = plan_moments(tree, s);  // host lists now: K2 below never waits on the host
-    if (weights_ready) ST_CUDA(cudaStreamWaitEvent(s, weights_ready, 0));
-    DevArray<unsigned long long> vflags(6, s);
+    // Validation and the tree-ordered source records on the second stream: only the near
+    // field (and the moments after them there) read the records, so they overlap the
+    // target ordering, the shard cut and the plan walks on s (launch_eval waits for `erec`
+    // before the near field's evaluation).
+    e1.record(s);  // the tree (positions only)
+    ST_CUDA(cudaStreamWaitEvent(aux.s, e1.e, 0));
+    if (weights_ready) ST_CUDA(cudaStreamWaitEvent(aux.s, weights_ready, 0));
+    DevArray<unsigned long long> vflags(6, aux.s);
     vflags.fill_bytes(0xff);
-    k_validate<<<nblocks(n, 256), 256, 0, s>>>(n, src.pos, sto ? src.f : nullptr, str ? src.h : nullptr,
-                                                str ? src.nu : nullptr, str ? 1 : 0, vflags.get());
+    k_validate<<<nblocks(n, 256), 256, 0, aux.s>>>(n, src.pos, sto ? src.f : nullptr, str ? src.h : nullptr,
+                                                    str ? src.nu : nullptr, str ? 1 : 0, vflags.get());
     ST_LAUNCH("k_validate");
     if (d_targets) {
-        k_validate<<<nblocks(nt_in, 256), 256, 0, s>>>(nt_in, d_targets, nullptr, nullptr, nullptr, 0, vflags.get() + 5);
+        k_validate<<<nblocks(nt_in, 256), 256, 0, aux.s>>>(nt_in, d_targets, nullptr, nullptr, nullptr, 0,
+                                                            vflags.get() + 5);
         ST_LAUNCH("k_validate");
     }
     count_launch(d_targets ? 2 : 1);
-    DevArray<double> rec(12 * n, s);
+    DevArray<double> rec(12 * n, aux.s);
     const DevArray<uint32_t>& to_tree = tree.to_tree;
-    k_pack_tree<<<nblocks(n, 256), 256, 0, s>>>(n, to_tree.get(), src.pos, sto ? src.f : nullptr,
-                                                str ? src.h : nullptr, str ? src.nu : nullptr, rec.get());
+    k_pack_tree<<<nblocks(n, 256), 256, 0, aux.s>>>(n, to_tree.get(), src.pos, sto ? src.f : nullptr,
+                                                    str ? src.h : nullptr, str ? src.nu : nullptr, rec.get());
     ST_LAUNCH("k_pack_tree");
     count_launch();
-    e1.record(s);
+    Event erec;
+    erec.record(aux.s);
 
     // K2: moments at order p, folded into the far-field weights, on the second stream: only
     // the far field needs them, so they overlap the plan walks and the near field
     // (launch_eval waits for `e2` before the far kernels).
-    ST_CUDA(cudaStreamWaitEvent(aux.s, e1.e, 0));
     Event em;
     em.record(aux.s);
     DevArray<double> M, W;
@@ -567,7 +574,8 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     fo.out = d_out;
     EvalTimes tm;
     tm.origin = e0.e;
-    launch_eval(sto, str, a, &fo, 1, s, &tm, e2.e, split ? &complete_weights : nullptr);
+    launch_eval(sto, str, a, &fo, 1, s, &tm, e2.e, split ? &complete_weights : nullptr, erec.e);
+    ST_CUDA(cudaStreamWaitEvent(s, erec.e, 0));  // vflags (read below) were written on aux
     e3.record(s);
 
     ST_CUDA(cudaMemcpyAsync(&ro.domain_err, d_err.get(), sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -59,9 +59,11 @@ struct EvalTimes {
 // before_far (if set): called once, after the first slab's near field is queued and
 // before any far kernel (also for an empty shard): the split moment pass completes W
 // there (exchange with the other ranks, top levels; capi.cu run_treecode).
+// src_ready (if set): the source records a.src are written on another stream; the near
+// field's evaluation waits for it (the plan walks before it do not read them).
 void launch_eval(bool sto, bool str, const TravArgs& a, const FarOrder* orders, int n_orders, cudaStream_t s,
                  EvalTimes* times = nullptr, cudaEvent_t far_ready = nullptr,
-                 const std::function<void()>* before_far = nullptr);
+                 const std::function<void()>* before_far = nullptr, cudaEvent_t src_ready = nullptr);
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);

@@ -13,6 +13,9 @@
 // Geometry uses the reference's exact non-FMA expressions (__dadd_rn /
 // __dmul_rn), and min / max / max-of-norm2 are order-free exact reductions.
 #include <algorithm>
+#include <cstdio>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "scan.cuh"
@@ -551,6 +554,15 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     if (n_sz >= 0x7fffffffull) fail(ST_INVALID_ARGUMENT, "build_tree: more than 2^31-1 particles");
     const uint32_t n = (uint32_t)n_sz;
     const int ntiles = (int)blocks(n, kTile);
+    // ST_DEBUG_BUILD=1: device-time marks of the build's phases (stderr)
+    static const bool dbg = getenv("ST_DEBUG_BUILD") != nullptr;
+    std::vector<std::pair<const char*, Event>> marks;
+    auto mark = [&](const char* what) {
+        if (!dbg) return;
+        marks.emplace_back(what, Event());
+        marks.back().second.record(s);
+    };
+    mark("start");
 
     // BFS node storage (grown per level)
     size_t cap = 64;
@@ -577,6 +589,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     k_iota<<<blocks(n, 256), 256, 0, s>>>(perm.get(), n);  // cluster_tree.hpp:160-161
     ST_LAUNCH("k_iota");
     count_launch();
+    mark("root");
 
     DevArray<int32_t> seg_of(n, s);
     DevArray<uint8_t> slot8(n, s);
@@ -652,6 +665,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         total += C;
         m = m2;
         ++depth;
+        mark("level");
     }
     level_start.push_back(total);
     const int T = total;
@@ -672,6 +686,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         count_launch();
     }
 
+    mark("subtree+preorder");
     out.n = n;
     out.ncl = T;
     out.depth = L - 1;
@@ -731,6 +746,19 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     ST_LAUNCH("k_invperm");
     count_launch();
     out.perm = std::move(perm);
+    mark("geometry+finalize");
+    if (dbg) {
+        ST_CUDA(cudaStreamSynchronize(s));
+        std::string line = "[build] n " + std::to_string(n) + " levels " + std::to_string(depth) + ":";
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            ST_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].second.e, marks[i].second.e));
+            char buf[64];
+            snprintf(buf, sizeof buf, " %s %.3f", marks[i].first, ms);
+            line += buf;
+        }
+        fprintf(stderr, "%s ms\n", line.c_str());
+    }
 }
 
 void order_targets(const double* d_pos, size_t n, cudaStream_t s, DevArray<uint32_t>& perm) {
