@@ -588,6 +588,9 @@ inline VelocityResult treecode_velocity_at_points(const ParticleSet& ps, const s
                                                   const TreecodeParams& params) {
     return detail::run(ps, &targets, params);
 }
+// New: give the device memory the library keeps between calls (its private pool, the near
+// field's workspace) on the current device back to the driver (st_release_workspace).
+inline void release_workspace() { abi::check(st_release_workspace()); }
 
 // ------------------------------------------------------------------ error_metric.hpp
 inline double relative_error(std::span<const Vec3> u_ref, std::span<const Vec3> u_test) {

@@ -435,9 +435,73 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     Event erec;
     erec.record(aux.s);
 
+    // batch order of the targets: 63-bit Morton order in their tight box (one radix sort,
+    // done on the second stream above)
+    ST_CUDA(cudaStreamWaitEvent(s, esort.e, 0));
+    DevArray<double> tx(3 * nt, s), ufar(3 * nt, s);
+    DevArray<uint32_t> torig(nt, s), tskip(nt, s);
+    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr,
+                                               tx.get(), torig.get(), tskip.get());
+    ST_LAUNCH("k_targets");
+    count_launch();
+    Event et, ec;  // timeline: targets ordered, shard cuts known
+    et.record(s);
+
+    DevArray<unsigned long long> d_stats(3, s);
+    DevArray<int> d_err(1, s), d_work(2, s);
+    d_stats.zero();
+    d_err.zero();
+
+    TravArgs a;
+    a.tx = tx.get();
+    a.tskip = tskip.get();
+    a.torig = torig.get();
+    a.nt = (int)nt;
+    const int nwarps = (int)((nt + 31) / 32);
+    a.w0 = 0;
+    a.w1 = nwarps;
+    a.geom = tree.geom.get();
+    a.info = tree.info.get();
+    a.ncl = tree.ncl;
+    a.th2 = prm.theta * prm.theta;
+    a.src = rec.get();
+    a.out = d_out;
+    a.per_target = d_per_target;
+    a.stats = d_stats.get();
+    a.err = d_err.get();
+    a.out_batch = out_batch ? 1 : 0;
+    a.work = d_work.get();
+    const int P = prm.order + (str ? 2 : 1);
+
+    if (nshards > 1) {
+        // work-balanced contiguous warp ranges, identical on every rank (deterministic)
+        DevArray<float> cost(nwarps, s);
+        a.warp_cost = cost.get();
+        // a dense far event costs ~8 (P+1)^2 warp DP instructions; a near (lane, source)
+        // pair ~1 (30 per 32 lanes)
+        a.sparse_max = far_sparse_max();
+        const float cf = (float)((P + 1) * (P + 1) * 8), cn = 1.f;
+        launch_count(a, cf, cn, s);
+        std::vector<float> hc(nwarps);
+        ST_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), sizeof(float) * nwarps, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        const int stride = count_stride(nwarps);
+        for (int w = 0; w < nwarps; ++w)  // every stride-th warp was sampled
+            if (w % stride) hc[w] = hc[w - w % stride];
+        std::vector<double> w(hc.begin(), hc.end());
+        std::vector<size_t> cuts(nshards + 1);
+        shard_cuts_host(nwarps, w.data(), nshards, cuts.data());
+        a.w0 = (int)cuts[shard];
+        a.w1 = (int)cuts[shard + 1];
+        a.warp_cost = nullptr;
+    }
+    ec.record(s);
+
     // K2: moments at order p, folded into the far-field weights, on the second stream: only
     // the far field needs them, so they overlap the plan walks and the near field
-    // (launch_eval waits for `e2` before the far kernels).
+    // (launch_eval waits for `e2` before the far kernels).  Queued after the target order
+    // and the shard cut: its host-side plan lists are pageable uploads, which wait for the
+    // second stream to drain (the record pack) -- s must have its work queued by then.
     Event em;
     em.record(aux.s);
     DevArray<double> M, W;
@@ -503,68 +567,6 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         compute_moments_device(tree, rec.get(), prm.order, sto, str, s, M, &top, true);
         fold_weights_rows_device(M.get(), d_top.get(), (int)sp.top_ids.size(), prm.order, sto, str, s, W.get());
     };
-
-    // batch order of the targets: 63-bit Morton order in their tight box (one radix sort,
-    // done on the second stream above)
-    ST_CUDA(cudaStreamWaitEvent(s, esort.e, 0));
-    DevArray<double> tx(3 * nt, s), ufar(3 * nt, s);
-    DevArray<uint32_t> torig(nt, s), tskip(nt, s);
-    k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr,
-                                               tx.get(), torig.get(), tskip.get());
-    ST_LAUNCH("k_targets");
-    count_launch();
-    Event et, ec;  // timeline: targets ordered, shard cuts known
-    et.record(s);
-
-    DevArray<unsigned long long> d_stats(3, s);
-    DevArray<int> d_err(1, s), d_work(2, s);
-    d_stats.zero();
-    d_err.zero();
-
-    TravArgs a;
-    a.tx = tx.get();
-    a.tskip = tskip.get();
-    a.torig = torig.get();
-    a.nt = (int)nt;
-    const int nwarps = (int)((nt + 31) / 32);
-    a.w0 = 0;
-    a.w1 = nwarps;
-    a.geom = tree.geom.get();
-    a.info = tree.info.get();
-    a.ncl = tree.ncl;
-    a.th2 = prm.theta * prm.theta;
-    a.src = rec.get();
-    a.out = d_out;
-    a.per_target = d_per_target;
-    a.stats = d_stats.get();
-    a.err = d_err.get();
-    a.out_batch = out_batch ? 1 : 0;
-    a.work = d_work.get();
-    const int P = prm.order + (str ? 2 : 1);
-
-    if (nshards > 1) {
-        // work-balanced contiguous warp ranges, identical on every rank (deterministic)
-        DevArray<float> cost(nwarps, s);
-        a.warp_cost = cost.get();
-        // a dense far event costs ~8 (P+1)^2 warp DP instructions; a near (lane, source)
-        // pair ~1 (30 per 32 lanes)
-        a.sparse_max = far_sparse_max();
-        const float cf = (float)((P + 1) * (P + 1) * 8), cn = 1.f;
-        launch_count(a, cf, cn, s);
-        std::vector<float> hc(nwarps);
-        ST_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), sizeof(float) * nwarps, cudaMemcpyDeviceToHost, s));
-        ST_CUDA(cudaStreamSynchronize(s));
-        const int stride = count_stride(nwarps);
-        for (int w = 0; w < nwarps; ++w)  // every stride-th warp was sampled
-            if (w % stride) hc[w] = hc[w - w % stride];
-        std::vector<double> w(hc.begin(), hc.end());
-        std::vector<size_t> cuts(nshards + 1);
-        shard_cuts_host(nwarps, w.data(), nshards, cuts.data());
-        a.w0 = (int)cuts[shard];
-        a.w1 = (int)cuts[shard + 1];
-        a.warp_cost = nullptr;
-    }
-    ec.record(s);
 
     a.sparse_max = far_sparse_max();
     FarOrder fo;

@@ -53,9 +53,25 @@ struct Event {
     void record(cudaStream_t s) { ST_CUDA(cudaEventRecord(e, s)); }
 };
 // A non-blocking stream owned by one call (destroyed after its queued work completes).
+// ST_AUX_PRIORITY=1: the second stream gets the device's highest priority (the moment pass
+// then finishes before the near field's persistent CTAs take every SM, but starves the
+// target order and the plan walks instead: measured zero-sum, r02o); default priority.
+inline int aux_priority() {
+    static const int v = [] {
+        const char* e = getenv("ST_AUX_PRIORITY");
+        if (!e || e[0] != '1') return 0;
+        int least = 0, greatest = 0;
+        if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return greatest;
+    }();
+    return v;
+}
 struct AuxStream {
     cudaStream_t s = nullptr;
-    AuxStream() { ST_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    AuxStream() { ST_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, aux_priority())); }
     AuxStream(const AuxStream&) = delete;
     AuxStream& operator=(const AuxStream&) = delete;
     ~AuxStream() {

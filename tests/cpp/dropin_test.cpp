@@ -122,6 +122,10 @@ static void device_checks() {
         const VelocityResult b = parallel_velocity(ps, p);
         CHECK(std::memcmp(a.velocity.data(), b.velocity.data(), a.velocity.size() * sizeof(Vec3)) == 0);
         CHECK(a.stats.direct_pairs == b.stats.direct_pairs);
+        // the library's cached device memory can be released between calls
+        release_workspace();
+        const VelocityResult c = parallel_velocity(ps, p);
+        CHECK(std::memcmp(a.velocity.data(), c.velocity.data(), a.velocity.size() * sizeof(Vec3)) == 0);
     }
     // stored radius equals brute force recomputation (test_cluster_tree.cpp:103-114)
     {
