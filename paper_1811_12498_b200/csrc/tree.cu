@@ -159,11 +159,11 @@ __global__ void k_root(const unsigned long long* __restrict__ mm, uint32_t n, ui
 }
 
 // Active segments of this level: range + geometric midpoint (cluster_tree.hpp:99).
-__global__ void k_mkseg(const int32_t* __restrict__ act, const int32_t* __restrict__ st,
-                        const uint32_t* __restrict__ nb_begin, const uint32_t* __restrict__ nb_end,
-                        const double* __restrict__ nb_box, uint32_t* seg_begin, uint32_t* seg_end, double* seg_mid) {
+__global__ void k_mkseg(const int32_t* __restrict__ act, int m, const uint32_t* __restrict__ nb_begin,
+                        const uint32_t* __restrict__ nb_end, const double* __restrict__ nb_box,
+                        uint32_t* seg_begin, uint32_t* seg_end, double* seg_mid) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= st[0]) return;
+    if (s >= m) return;
     const int v = act[s];
     seg_begin[s] = nb_begin[v];
     seg_end[s] = nb_end[v];
@@ -173,11 +173,9 @@ __global__ void k_mkseg(const int32_t* __restrict__ act, const int32_t* __restri
 
 // Element -> active segment (segments are disjoint and sorted by begin).
 __global__ void k_segof(uint32_t n, const uint32_t* __restrict__ seg_begin,
-                        const uint32_t* __restrict__ seg_end, const int32_t* __restrict__ st,
-                        int32_t* __restrict__ seg_of) {
+                        const uint32_t* __restrict__ seg_end, int m, int32_t* __restrict__ seg_of) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = st[0];
-    if (i >= n || m == 0) return;
+    if (i >= n) return;
     int lo = 0, hi = m - 1, found = -1;
     while (lo <= hi) {
         const int mid = (lo + hi) >> 1;
@@ -194,10 +192,9 @@ __global__ void k_segof(uint32_t n, const uint32_t* __restrict__ seg_begin,
 // Octant slot, ties go to the upper child (cluster_tree.hpp:101-105), and per-tile
 // histograms.  slot 8 marks elements outside every active segment.
 __global__ void __launch_bounds__(kTileThreads)
-    k_slot_hist(uint32_t n, const int32_t* __restrict__ st, const double* __restrict__ pos,
-                const uint32_t* __restrict__ perm, const int32_t* __restrict__ seg_of,
-                const double* __restrict__ seg_mid, uint8_t* __restrict__ slot8, uint32_t* __restrict__ blk_cnt) {
-    if (st[0] == 0) return;  // a level queued past the last one
+    k_slot_hist(uint32_t n, const double* __restrict__ pos, const uint32_t* __restrict__ perm,
+                const int32_t* __restrict__ seg_of, const double* __restrict__ seg_mid,
+                uint8_t* __restrict__ slot8, uint32_t* __restrict__ blk_cnt) {
     // counts by warp ballots (lane k keeps the warp's count of slot k), one shared atomic
     // per warp and slot: 8 contended shared-memory counters per element were the kernel's
     // bottleneck
@@ -232,13 +229,13 @@ __global__ void __launch_bounds__(kTileThreads)
 
 // Global exclusive per-slot prefix P[pos][k] at both ends of every active segment
 // (one warp per segment): seg_base[s][k] = P[begin][k], seg_cnt[s][k] = P[end][k] - P[begin][k].
-__global__ void k_segbase(const int32_t* __restrict__ st, const uint32_t* __restrict__ seg_begin,
+__global__ void k_segbase(int m, const uint32_t* __restrict__ seg_begin,
                           const uint32_t* __restrict__ seg_end, const uint8_t* __restrict__ slot8,
                           const uint32_t* __restrict__ blk_off, uint32_t* __restrict__ seg_base,
                           uint32_t* __restrict__ seg_cnt) {
     const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (s >= st[0]) return;  // whole warps only; no block-level barrier below
+    if (s >= m) return;  // whole warps only; no block-level barrier below
     uint32_t P[2] = {0, 0};
     for (int which = 0; which < 2; ++which) {
         const uint32_t p = which ? seg_end[s] : seg_begin[s];
@@ -266,16 +263,10 @@ __global__ void k_segbase(const int32_t* __restrict__ st, const uint32_t* __rest
 
 // Stable scatter: new position = segment begin + child offset + stable rank.
 __global__ void __launch_bounds__(kTileThreads)
-    k_scatter(uint32_t n, const int32_t* __restrict__ st, const uint8_t* __restrict__ slot8,
-              const int32_t* __restrict__ seg_of,
+    k_scatter(uint32_t n, const uint8_t* __restrict__ slot8, const int32_t* __restrict__ seg_of,
               const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ seg_begin,
               const uint32_t* __restrict__ seg_base, const uint32_t* __restrict__ seg_cnt,
               const uint32_t* __restrict__ perm_in, uint32_t* __restrict__ perm_out) {
-    if (st[0] == 0) {  // a level queued past the last one: the order stays (the host swaps buffers)
-        const uint32_t base = blockIdx.x * kTile;
-        for (uint32_t i = base + threadIdx.x; i < min(n, base + kTile); i += kTileThreads) perm_out[i] = perm_in[i];
-        return;
-    }
     __shared__ uint32_t warp_cnt[kTileThreads / 32][8];
     __shared__ uint32_t run[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -320,27 +311,23 @@ __global__ void __launch_bounds__(kTileThreads)
     }
 }
 
-// children per segment; zero up to the level's bound mb so the scan over mb entries is exact
-__global__ void k_nch(const int32_t* __restrict__ st, int mb, const uint32_t* __restrict__ seg_cnt,
-                      int32_t* __restrict__ nch) {
+__global__ void k_nch(int m, const uint32_t* __restrict__ seg_cnt, int32_t* __restrict__ nch) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= mb) return;
+    if (s >= m) return;
     int c = 0;
-    if (s < st[0])
-        for (int k = 0; k < 8; ++k) c += seg_cnt[s * 8 + k] != 0;
+    for (int k = 0; k < 8; ++k) c += seg_cnt[s * 8 + k] != 0;
     nch[s] = c;
 }
 
 // Child clusters in slot order (cluster_tree.hpp:125-137), empty slots pruned.
-__global__ void k_children(const int32_t* __restrict__ st, const int32_t* __restrict__ act,
-                           const uint32_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_cnt,
-                           const int32_t* __restrict__ chbase, int n0, const double* box_in, double* nb_box,
-                           uint32_t* __restrict__ nb_begin, uint32_t* __restrict__ nb_end,
-                           int32_t* __restrict__ nb_first, int32_t* __restrict__ nb_nch,
-                           int32_t* __restrict__ act_flag) {
+__global__ void k_children(int m, const int32_t* __restrict__ act, const uint32_t* __restrict__ seg_begin,
+                           const uint32_t* __restrict__ seg_cnt, const int32_t* __restrict__ chbase,
+                           int next_start, int n0, int child_depth, const double* box_in,
+                           double* nb_box, uint32_t* __restrict__ nb_begin,
+                           uint32_t* __restrict__ nb_end, int32_t* __restrict__ nb_first,
+                           int32_t* __restrict__ nb_nch, int32_t* __restrict__ act_flag) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= st[0]) return;
-    const int next_start = st[1], child_depth = st[2] + 1;
+    if (s >= m) return;
     const int v = act[s];
     double glo[3], ghi[3], mid[3];
     for (int a = 0; a < 3; ++a) {
@@ -371,32 +358,10 @@ __global__ void k_children(const int32_t* __restrict__ st, const int32_t* __rest
     }
 }
 
-__global__ void k_compact(const int32_t* __restrict__ st, const int32_t* __restrict__ chbase,
-                          const int32_t* __restrict__ flag, const int32_t* __restrict__ pos,
-                          int32_t* __restrict__ act) {
+__global__ void k_compact(int C, int next_start, const int32_t* __restrict__ flag,
+                          const int32_t* __restrict__ pos, int32_t* __restrict__ act) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < chbase[st[0]] && flag[c]) act[pos[c]] = st[1] + c;
-}
-
-// End of a level: its first cluster id, then the state of the next level
-// st = {splitting segments, clusters so far, depth} and a copy {m, total, C} the host reads
-// two levels later (the level loop never waits for the level it has just queued).
-__global__ void k_level_end(int32_t* __restrict__ st, const int32_t* __restrict__ chbase,
-                            const int32_t* __restrict__ fpos, int cmax, int32_t* __restrict__ rec) {
-    const int m = st[0], total = st[1];
-    const int C = chbase[m], m2 = fpos[cmax];
-    rec[0] = m2;
-    rec[1] = total + C;
-    rec[2] = C;
-    st[0] = m2;
-    st[1] = total + C;
-    st[2] += 1;
-}
-
-__global__ void k_level_init(int32_t* __restrict__ st, int m0) {
-    st[0] = m0;
-    st[1] = 1;
-    st[2] = 0;
+    if (c < C && flag[c]) act[pos[c]] = next_start + c;
 }
 
 __global__ void k_subtree(int v0, int v1, const int32_t* __restrict__ first,
@@ -630,116 +595,80 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     DevArray<uint8_t> slot8(n, s);
     DevArray<uint32_t> blk_cnt((size_t)ntiles * 8, s), blk_off((size_t)(ntiles + 1) * 8, s);
 
-    // The level loop runs on device-resident state (k_level_end): no level waits for the
-    // host.  Each level's work is sized by a bound the host knows from two levels back
-    // (splitting segments m_d <= 8 m_(d-1), at most N / (N0 + 1); children C_d <= 8 m_d),
-    // the kernels read the exact counts on the device, and the host reads level d-2's
-    // counts (an event wait the GPU is already past) before queuing level d.  A level
-    // queued after the last real one finds m = 0 and does nothing.
-    const int m0 = n > (uint32_t)n0 ? 1 : 0;
-    const long long mcap = (long long)n / ((long long)n0 + 1) + 1;  // disjoint segments of > N0
-    constexpr int kMaxLevels = 66;                                   // depth <= 64, + 1 spare
-    DevArray<int32_t> dst(3, s), drec(3 * kMaxLevels, s);
-    k_level_init<<<1, 1, 0, s>>>(dst.get(), m0);
-    ST_LAUNCH("k_level_init");
-    count_launch();
-    thread_local int32_t* hrec = nullptr;  // pinned: the levels' {m, total, C}
-    if (!hrec) ST_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hrec), sizeof(int32_t) * 3 * kMaxLevels));
-    std::vector<Event> lev_ev;
-    lev_ev.reserve(kMaxLevels);
-    std::vector<int> m_in{m0}, tot_in{1};  // exact values, filled as the host learns them
-    DevArray<int32_t> act(std::max(m0, 1), s);
-    if (m0) ST_CUDA(cudaMemsetAsync(act.get(), 0, sizeof(int32_t), s));
-    int queued = 0;
-    for (int d = 0; m0 && d < kMaxLevels; ++d) {
-        // learn m_in[d-1], tot_in[d-1] (level d-2's record); the GPU is past that point or
-        // busy with level d-1.  If level d-1 has already finished too, its record gives the
-        // exact m_in[d] (no level is queued past the last one).
-        while ((int)m_in.size() < d) {
-            const int k = (int)m_in.size() - 1;  // record of level k
-            ST_CUDA(cudaEventSynchronize(lev_ev[k].e));
-            m_in.push_back(hrec[3 * k]);
-            tot_in.push_back(hrec[3 * k + 1]);
-        }
-        if (d >= 1 && (int)m_in.size() == d) {
-            const cudaError_t q = cudaEventQuery(lev_ev[d - 1].e);
-            if (q == cudaSuccess) {
-                m_in.push_back(hrec[3 * (d - 1)]);
-                tot_in.push_back(hrec[3 * (d - 1) + 1]);
-            } else if (q != cudaErrorNotReady) {
-                cuda_check(q, "cudaEventQuery");
-            }
-        }
-        if ((int)m_in.size() > d && m_in[d] == 0) break;  // nothing left to split
-        const int prev = std::max(d - 1, 0);
-        if (m_in[prev] == 0) break;  // level d-1 had nothing to split: done
-        const bool exact = (int)m_in.size() > d;
-        const int mb = exact ? m_in[d] : (int)std::min<long long>(mcap, 8LL * m_in[prev]);
-        const int cmax = 8 * mb;
-        const size_t tot_bound = exact ? (size_t)tot_in[d] : (size_t)tot_in[prev] + 8 * (size_t)m_in[prev];
-        DevArray<uint32_t> seg_begin(mb, s), seg_end(mb, s), seg_base((size_t)8 * mb, s), seg_cnt((size_t)8 * mb, s);
-        DevArray<double> seg_mid((size_t)3 * mb, s);
-        DevArray<int32_t> nch(mb, s), chbase(mb + 1, s);
+    std::vector<int> level_start{0};
+    int total = 1;
+    int m = n > (uint32_t)n0 ? 1 : 0;
+    DevArray<int32_t> act(std::max(m, 1), s);
+    if (m) ST_CUDA(cudaMemsetAsync(act.get(), 0, sizeof(int32_t), s));
+    int depth = 0;
 
-        k_mkseg<<<blocks(mb, 128), 128, 0, s>>>(act.get(), dst.get(), nb_begin.get(), nb_end.get(), nb_box.get(),
-                                                seg_begin.get(), seg_end.get(), seg_mid.get());
+    while (m > 0) {
+        DevArray<uint32_t> seg_begin(m, s), seg_end(m, s), seg_base((size_t)8 * m, s),
+            seg_cnt((size_t)8 * m, s);
+        DevArray<double> seg_mid((size_t)3 * m, s);
+        DevArray<int32_t> nch(m, s), chbase(m + 1, s);
+
+        k_mkseg<<<blocks(m, 128), 128, 0, s>>>(act.get(), m, nb_begin.get(), nb_end.get(), nb_box.get(),
+                                               seg_begin.get(), seg_end.get(), seg_mid.get());
         ST_LAUNCH("k_mkseg");
-        k_segof<<<blocks(n, 256), 256, 0, s>>>(n, seg_begin.get(), seg_end.get(), dst.get(), seg_of.get());
+        k_segof<<<blocks(n, 256), 256, 0, s>>>(n, seg_begin.get(), seg_end.get(), m, seg_of.get());
         ST_LAUNCH("k_segof");
-        k_slot_hist<<<ntiles, kTileThreads, 0, s>>>(n, dst.get(), d_pos, perm.get(), seg_of.get(), seg_mid.get(),
+        k_slot_hist<<<ntiles, kTileThreads, 0, s>>>(n, d_pos, perm.get(), seg_of.get(), seg_mid.get(),
                                                     slot8.get(), blk_cnt.get());
         ST_LAUNCH("k_slot_hist");
         launch_scan_cols(blk_cnt.get(), blk_off.get(), ntiles, 8, s);
-        k_segbase<<<blocks((size_t)2 * mb * 32, 256), 256, 0, s>>>(dst.get(), seg_begin.get(), seg_end.get(),
-                                                                   slot8.get(), blk_off.get(), seg_base.get(),
-                                                                   seg_cnt.get());
+        k_segbase<<<blocks((size_t)2 * m * 32, 256), 256, 0, s>>>(m, seg_begin.get(), seg_end.get(),
+                                                                  slot8.get(), blk_off.get(),
+                                                                  seg_base.get(), seg_cnt.get());
         ST_LAUNCH("k_segbase");
-        k_scatter<<<ntiles, kTileThreads, 0, s>>>(n, dst.get(), slot8.get(), seg_of.get(), blk_off.get(),
+        k_scatter<<<ntiles, kTileThreads, 0, s>>>(n, slot8.get(), seg_of.get(), blk_off.get(),
                                                   seg_begin.get(), seg_base.get(), seg_cnt.get(),
                                                   perm.get(), perm2.get());
         ST_LAUNCH("k_scatter");
         perm.swap(perm2);
-        k_nch<<<blocks(mb, 128), 128, 0, s>>>(dst.get(), mb, seg_cnt.get(), nch.get());
+        k_nch<<<blocks(m, 128), 128, 0, s>>>(m, seg_cnt.get(), nch.get());
         ST_LAUNCH("k_nch");
-        launch_scan_i32(nch.get(), chbase.get(), mb, s);
+        launch_scan_i32(nch.get(), chbase.get(), m, s);
         count_launch(6);
-        const size_t need = tot_bound + (size_t)cmax;
-        grow(nb_begin, need, tot_bound, s);
-        grow(nb_end, need, tot_bound, s);
-        grow(nb_first, need, tot_bound, s);
-        grow(nb_nch, need, tot_bound, s);
-        grow(nb_box, 6 * need, 6 * tot_bound, s);
+        // sized by the bound C <= 8m so the children are made without waiting for C; one
+        // host round trip per level reads C and the next level's split count together
+        const int Cmax = 8 * m;
+        const size_t need = (size_t)total + Cmax;
+        grow(nb_begin, need, total, s);
+        grow(nb_end, need, total, s);
+        grow(nb_first, need, total, s);
+        grow(nb_nch, need, total, s);
+        grow(nb_box, 6 * need, 6 * (size_t)total, s);
 
-        DevArray<int32_t> flag(cmax, s), fpos(cmax + 1, s);
-        ST_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t) * cmax, s));
-        k_children<<<blocks(mb, 128), 128, 0, s>>>(dst.get(), act.get(), seg_begin.get(), seg_cnt.get(),
-                                                   chbase.get(), n0, nb_box.get(), nb_box.get(), nb_begin.get(),
-                                                   nb_end.get(), nb_first.get(), nb_nch.get(), flag.get());
+        DevArray<int32_t> flag(Cmax, s), fpos(Cmax + 1, s);
+        ST_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t) * Cmax, s));
+        k_children<<<blocks(m, 128), 128, 0, s>>>(m, act.get(), seg_begin.get(), seg_cnt.get(),
+                                                  chbase.get(), total, n0, depth + 1, nb_box.get(),
+                                                  nb_box.get(), nb_begin.get(), nb_end.get(),
+                                                  nb_first.get(), nb_nch.get(), flag.get());
         ST_LAUNCH("k_children");
-        launch_scan_i32(flag.get(), fpos.get(), cmax, s);
-        DevArray<int32_t> act2(cmax, s);
-        k_compact<<<blocks(cmax, 256), 256, 0, s>>>(dst.get(), chbase.get(), flag.get(), fpos.get(), act2.get());
-        ST_LAUNCH("k_compact");
-        k_level_end<<<1, 1, 0, s>>>(dst.get(), chbase.get(), fpos.get(), cmax, drec.get() + 3 * d);
-        ST_LAUNCH("k_level_end");
-        count_launch(3);
-        ST_CUDA(cudaMemcpyAsync(hrec + 3 * d, drec.get() + 3 * d, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        lev_ev.emplace_back();
-        lev_ev.back().record(s);
+        launch_scan_i32(flag.get(), fpos.get(), Cmax, s);
+        count_launch();
+        int32_t cm[2] = {0, 0};  // C, next level's split count
+        ST_CUDA(cudaMemcpyAsync(&cm[0], chbase.get() + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaMemcpyAsync(&cm[1], fpos.get() + Cmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        const int C = cm[0], m2 = cm[1];
+        DevArray<int32_t> act2(std::max(m2, 1), s);
+        if (m2) {
+            k_compact<<<blocks(C, 256), 256, 0, s>>>(C, total, flag.get(), fpos.get(), act2.get());
+            ST_LAUNCH("k_compact");
+            count_launch();
+        }
         act = std::move(act2);
-        queued = d + 1;
+        level_start.push_back(total);
+        total += C;
+        m = m2;
+        ++depth;
         mark("level");
     }
-    // every queued level's record: the real levels end at the first m = 0
-    if (queued) ST_CUDA(cudaEventSynchronize(lev_ev[queued - 1].e));
-    std::vector<int> level_start{0, 1};  // level d holds clusters [level_start[d], level_start[d+1])
-    int depth = 0;
-    for (int d = 0, mcur = m0; d < queued && mcur > 0; ++d) {
-        level_start.push_back(hrec[3 * d + 1]);
-        mcur = hrec[3 * d];
-        ++depth;
-    }
-    const int T = level_start.back();
+    level_start.push_back(total);
+    const int T = total;
     const int L = (int)level_start.size() - 1;
 
     DevArray<int32_t> size(T, s), pre(T, s);
