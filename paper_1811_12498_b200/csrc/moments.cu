@@ -305,11 +305,19 @@ template <bool STO, bool STR>
 __global__ void __launch_bounds__(kThreads)
     k_fold(int p, int P, int Estride, const double* __restrict__ M, double* __restrict__ W,
            const int32_t* __restrict__ rows) {
-    extern __shared__ double s_w[];  // [E(P)][4]
+    extern __shared__ double s_w[];  // [E(P)][4], then the cluster's moments [E(p)][12]
     const int EP = mi_count(P);
     const size_t blk = rows ? (size_t)rows[blockIdx.x] : (size_t)blockIdx.x;
-    // moments of order p are the graded prefix of any higher-order block (multi_index.hpp:110-114)
-    const double* Mb = M + blk * Estride * 12;
+    // moments of order p are the graded prefix of any higher-order block (multi_index.hpp:110-114);
+    // staged once with coalesced loads: the fold reads each ~12 times at scattered indices
+    double* sM = s_w + 4 * EP;
+    {
+        const double* g = M + blk * Estride * 12;
+        const int cnt = mi_count(p) * 12;
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) sM[i] = g[i];
+        __syncthreads();
+    }
+    const double* Mb = sM;
     const double third = 1.0 / 3.0;
 
     for (int q = threadIdx.x; q < EP; q += blockDim.x) {
@@ -692,7 +700,7 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
 void fold_weights_device(const double* M, int nblk, int p, bool sto, bool str, cudaStream_t s,
                          DevArray<double>& W, int pstride) {
     const int P = p + (str ? 2 : 1);
-    const size_t smem = sizeof(double) * 4 * mi_count(P);
+    const size_t smem = sizeof(double) * (4 * mi_count(P) + 12 * mi_count(p));
     W.alloc((size_t)nblk * harm_count(P) * 4, s);
     if (nblk == 0) return;
     auto go = [&](auto kern) {
@@ -710,7 +718,7 @@ void fold_weights_rows_device(const double* M, const int32_t* rows, int n, int p
                               cudaStream_t s, double* W) {
     if (n <= 0) return;
     const int P = p + (str ? 2 : 1);
-    const size_t smem = sizeof(double) * 4 * mi_count(P);
+    const size_t smem = sizeof(double) * (4 * mi_count(P) + 12 * mi_count(p));
     auto go = [&](auto kern) {
         ST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<n, kThreads, smem, s>>>(p, P, mi_count(p), M, W, rows);

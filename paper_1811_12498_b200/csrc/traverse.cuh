@@ -72,7 +72,18 @@ void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64
 constexpr int kCountStride = 4;
 // every count_stride(w)-th of w batch warps is walked for the shard cuts: at least every
 // 4th, at most ~8K samples (the per-warp cost is smooth along the Morton order)
-inline int count_stride(int warps) { return warps / 8192 > kCountStride ? warps / 8192 : kCountStride; }
+// ST_COUNT_SAMPLES overrides the ~8K sampled warps (A/B of the multi-GPU cut cost).
+inline int count_samples() {
+    static const int v = [] {
+        const char* e = getenv("ST_COUNT_SAMPLES");
+        const int k = e ? atoi(e) : 8192;
+        return k > 0 ? k : 8192;
+    }();
+    return v;
+}
+inline int count_stride(int warps) {
+    return warps / count_samples() > kCountStride ? warps / count_samples() : kCountStride;
+}
 void launch_count(const TravArgs& a, float far_cost, float near_cost, cudaStream_t s);
 
 // O(N^2) contracted direct sum (kernels.hpp:45-83, 123-150): sources are the
