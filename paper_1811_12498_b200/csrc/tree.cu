@@ -10,6 +10,10 @@
 //   seg_of -> slot + tile histogram -> column scan -> segment bases -> stable
 //   scatter -> children records -> compaction of the next active level,
 // followed by subtree sizes (bottom-up) and pre-order ids (top-down).
+// The first kKeyLevels levels skip the per-level passes over all points: one radix
+// sort of each point's octant digits (k_geokey) orders every node's range at once and a
+// level's children come from binary searches (k_split_sorted); a second sort restores
+// input order inside the leaves.  Levels below kKeyLevels use the partition passes.
 // Geometry uses the reference's exact non-FMA expressions (__dadd_rn /
 // __dmul_rn), and min / max / max-of-norm2 are order-free exact reductions.
 #include <algorithm>
@@ -517,6 +521,86 @@ __global__ void k_finalize(int T, int geometry, const int32_t* __restrict__ pre,
     }
 }
 
+// ---- keyed levels: one radix sort replaces the first kKeyLevels partition passes ----
+//
+// The reference's bisection is a pure function of the point and the root cube: at depth d
+// the octant is decided against the midpoint of the depth-d box, whose bounds are the
+// parent's bound or the parent's midpoint (cluster_tree.hpp:99-105, 125-137).  Each point
+// descends kKeyLevels levels with the same rn arithmetic as k_children / k_mkseg and
+// records its octant digits, most significant first.  A stable sort of these keys puts
+// every depth-d node (d <= kKeyLevels) into one contiguous, slot-ordered range, so a
+// level's children are found by binary search in the sorted keys instead of by a
+// histogram + scatter pass over all n points.  Inside a node at depth kKeyLevels the
+// points keep their input order (stable sort), which is what the partition passes
+// continue from if a node there still splits.  Inside a leaf the reference keeps input
+// order, which the key sort does not: k_leafkey + a second stable sort restore it.
+constexpr int kKeyLevels = 10;  // 30-bit keys
+
+__global__ void k_geokey(uint32_t n, const double* __restrict__ pos, const double* __restrict__ root_box,
+                         uint32_t* __restrict__ key, uint32_t* __restrict__ idx) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double lo[3], hi[3], p[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = root_box[a];
+        hi[a] = root_box[3 + a];
+        p[a] = pos[3 * (size_t)i + a];
+    }
+    uint32_t k = 0;
+#pragma unroll
+    for (int d = 0; d < kKeyLevels; ++d) {
+        uint32_t slot = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double mid = __dmul_rn(__dadd_rn(lo[a], hi[a]), 0.5);
+            const bool up = p[a] >= mid;
+            slot |= (up ? 1u : 0u) << a;
+            lo[a] = up ? mid : lo[a];
+            hi[a] = up ? hi[a] : mid;
+        }
+        k = (k << 3) | slot;
+    }
+    key[i] = k;
+    idx[i] = i;
+}
+
+// Children of the active segments at depth d < kKeyLevels from the sorted keys: 8 threads
+// per segment, thread k finds the first position whose depth-d digit is >= k.
+__global__ void k_split_sorted(int m, int d, const int32_t* __restrict__ act, const uint32_t* __restrict__ nb_begin,
+                               const uint32_t* __restrict__ nb_end, const uint32_t* __restrict__ skey,
+                               uint32_t* __restrict__ seg_begin, uint32_t* __restrict__ seg_cnt) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = g >> 3, k = g & 7;
+    const bool live = s < m;
+    const int v = live ? act[s] : 0;
+    const uint32_t b = live ? nb_begin[v] : 0, e = live ? nb_end[v] : 0;
+    const int sh = 3 * (kKeyLevels - 1 - d);
+    uint32_t lo = b, hi = e;  // first t in [b, e) with digit(t) >= k, else e
+    while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        if ((int)((skey[mid] >> sh) & 7u) < k) lo = mid + 1;
+        else hi = mid;
+    }
+    // the next slot's start (lane k + 1 of the same 8-group; e after slot 7)
+    const uint32_t nxt = __shfl_down_sync(0xffffffffu, lo, 1, 8);
+    if (!live) return;
+    const uint32_t end_k = k == 7 ? e : nxt;
+    seg_cnt[8 * s + k] = end_k - lo;
+    if (k == 0) seg_begin[s] = b;
+}
+
+// Leaf key of every point: the leaf's pre-order id (leaves in pre-order = tree order),
+// stored at the point's input index.  One warp per cluster; internal clusters skip.
+__global__ void k_leafkey(int T, const int32_t* __restrict__ nb_nch, const uint32_t* __restrict__ nb_begin,
+                          const uint32_t* __restrict__ nb_end, const int32_t* __restrict__ pre,
+                          const uint32_t* __restrict__ perm, uint32_t* __restrict__ lkey) {
+    const int v = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+    if (v >= T || nb_nch[v] != 0) return;
+    const uint32_t key = (uint32_t)pre[v];
+    for (uint32_t t = nb_begin[v] + (threadIdx.x & 31); t < nb_end[v]; t += 32) lkey[perm[t]] = key;
+}
+
 __global__ void k_iota(uint32_t* p, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = i;
@@ -585,15 +669,33 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     ST_CUDA(cudaMemsetAsync(nb_first.get(), 0xff, sizeof(int32_t), s));
     ST_CUDA(cudaMemsetAsync(nb_nch.get(), 0, sizeof(int32_t), s));
 
-    DevArray<uint32_t> perm(n, s), perm2(n, s);
-    k_iota<<<blocks(n, 256), 256, 0, s>>>(perm.get(), n);  // cluster_tree.hpp:160-161
-    ST_LAUNCH("k_iota");
-    count_launch();
+    // keyed levels (k_geokey): ST_TREE_PARTITION=1 forces the partition passes from the root
+    static const bool partition_only = getenv("ST_TREE_PARTITION") != nullptr;
+    const bool keyed = !partition_only && n > (uint32_t)n0;
+    DevArray<uint32_t> perm(n, s), perm2, skey;
+    if (keyed) {
+        DevArray<uint32_t> key(n, s), idx(n, s);
+        skey.alloc(n, s);
+        k_geokey<<<blocks(n, 256), 256, 0, s>>>(n, d_pos, nb_box.get(), key.get(), idx.get());
+        ST_LAUNCH("k_geokey");
+        size_t tmp = 0;
+        ST_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), skey.get(), idx.get(), perm.get(), (int)n, 0,
+                                                3 * kKeyLevels, s));
+        DevArray<char> scratch(tmp, s);
+        ST_CUDA(cub::DeviceRadixSort::SortPairs(scratch.get(), tmp, key.get(), skey.get(), idx.get(), perm.get(),
+                                                (int)n, 0, 3 * kKeyLevels, s));
+        count_launch(1 + 5);  // + the sort's passes
+    } else {
+        k_iota<<<blocks(n, 256), 256, 0, s>>>(perm.get(), n);  // cluster_tree.hpp:160-161
+        ST_LAUNCH("k_iota");
+        count_launch();
+    }
     mark("root");
 
-    DevArray<int32_t> seg_of(n, s);
-    DevArray<uint8_t> slot8(n, s);
-    DevArray<uint32_t> blk_cnt((size_t)ntiles * 8, s), blk_off((size_t)(ntiles + 1) * 8, s);
+    // partition-pass state, allocated only if a level below the keyed ones splits
+    DevArray<int32_t> seg_of;
+    DevArray<uint8_t> slot8;
+    DevArray<uint32_t> blk_cnt, blk_off;
 
     std::vector<int> level_start{0};
     int total = 1;
@@ -603,33 +705,52 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     int depth = 0;
 
     while (m > 0) {
-        DevArray<uint32_t> seg_begin(m, s), seg_end(m, s), seg_base((size_t)8 * m, s),
-            seg_cnt((size_t)8 * m, s);
-        DevArray<double> seg_mid((size_t)3 * m, s);
+        DevArray<uint32_t> seg_begin(m, s), seg_end, seg_base, seg_cnt((size_t)8 * m, s);
+        DevArray<double> seg_mid;
         DevArray<int32_t> nch(m, s), chbase(m + 1, s);
 
-        k_mkseg<<<blocks(m, 128), 128, 0, s>>>(act.get(), m, nb_begin.get(), nb_end.get(), nb_box.get(),
-                                               seg_begin.get(), seg_end.get(), seg_mid.get());
-        ST_LAUNCH("k_mkseg");
-        k_segof<<<blocks(n, 256), 256, 0, s>>>(n, seg_begin.get(), seg_end.get(), m, seg_of.get());
-        ST_LAUNCH("k_segof");
-        k_slot_hist<<<ntiles, kTileThreads, 0, s>>>(n, d_pos, perm.get(), seg_of.get(), seg_mid.get(),
-                                                    slot8.get(), blk_cnt.get());
-        ST_LAUNCH("k_slot_hist");
-        launch_scan_cols(blk_cnt.get(), blk_off.get(), ntiles, 8, s);
-        k_segbase<<<blocks((size_t)2 * m * 32, 256), 256, 0, s>>>(m, seg_begin.get(), seg_end.get(),
-                                                                  slot8.get(), blk_off.get(),
-                                                                  seg_base.get(), seg_cnt.get());
-        ST_LAUNCH("k_segbase");
-        k_scatter<<<ntiles, kTileThreads, 0, s>>>(n, slot8.get(), seg_of.get(), blk_off.get(),
-                                                  seg_begin.get(), seg_base.get(), seg_cnt.get(),
-                                                  perm.get(), perm2.get());
-        ST_LAUNCH("k_scatter");
-        perm.swap(perm2);
+        if (keyed && depth < kKeyLevels) {
+            k_split_sorted<<<blocks((size_t)8 * m, 128), 128, 0, s>>>(m, depth, act.get(), nb_begin.get(),
+                                                                      nb_end.get(), skey.get(), seg_begin.get(),
+                                                                      seg_cnt.get());
+            ST_LAUNCH("k_split_sorted");
+            count_launch();
+        } else {
+            if (!seg_of.size()) {
+                skey.reset();
+                seg_of.alloc(n, s);
+                slot8.alloc(n, s);
+                blk_cnt.alloc((size_t)ntiles * 8, s);
+                blk_off.alloc((size_t)(ntiles + 1) * 8, s);
+                perm2.alloc(n, s);
+            }
+            seg_end.alloc(m, s);
+            seg_base.alloc((size_t)8 * m, s);
+            seg_mid.alloc((size_t)3 * m, s);
+            k_mkseg<<<blocks(m, 128), 128, 0, s>>>(act.get(), m, nb_begin.get(), nb_end.get(), nb_box.get(),
+                                                   seg_begin.get(), seg_end.get(), seg_mid.get());
+            ST_LAUNCH("k_mkseg");
+            k_segof<<<blocks(n, 256), 256, 0, s>>>(n, seg_begin.get(), seg_end.get(), m, seg_of.get());
+            ST_LAUNCH("k_segof");
+            k_slot_hist<<<ntiles, kTileThreads, 0, s>>>(n, d_pos, perm.get(), seg_of.get(), seg_mid.get(),
+                                                        slot8.get(), blk_cnt.get());
+            ST_LAUNCH("k_slot_hist");
+            launch_scan_cols(blk_cnt.get(), blk_off.get(), ntiles, 8, s);
+            k_segbase<<<blocks((size_t)2 * m * 32, 256), 256, 0, s>>>(m, seg_begin.get(), seg_end.get(),
+                                                                      slot8.get(), blk_off.get(),
+                                                                      seg_base.get(), seg_cnt.get());
+            ST_LAUNCH("k_segbase");
+            k_scatter<<<ntiles, kTileThreads, 0, s>>>(n, slot8.get(), seg_of.get(), blk_off.get(),
+                                                      seg_begin.get(), seg_base.get(), seg_cnt.get(),
+                                                      perm.get(), perm2.get());
+            ST_LAUNCH("k_scatter");
+            perm.swap(perm2);
+            count_launch(5);
+        }
         k_nch<<<blocks(m, 128), 128, 0, s>>>(m, seg_cnt.get(), nch.get());
         ST_LAUNCH("k_nch");
         launch_scan_i32(nch.get(), chbase.get(), m, s);
-        count_launch(6);
+        count_launch(2);
         // sized by the bound C <= 8m so the children are made without waiting for C; one
         // host round trip per level reads C and the next level's split count together
         const int Cmax = 8 * m;
@@ -686,6 +807,30 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         count_launch();
     }
 
+    if (keyed) {
+        // inside each leaf, input order (the reference's stable partitions): sort the points
+        // by (leaf pre-order id, input index) -- a stable sort of the leaf ids over the
+        // input indices
+        seg_of.reset();
+        slot8.reset();
+        perm2.reset();
+        DevArray<uint32_t> lkey(n, s), lkey2(n, s), idx(n, s), perm_out(n, s);
+        k_leafkey<<<blocks((size_t)32 * T, 256), 256, 0, s>>>(T, nb_nch.get(), nb_begin.get(), nb_end.get(),
+                                                              pre.get(), perm.get(), lkey.get());
+        ST_LAUNCH("k_leafkey");
+        k_iota<<<blocks(n, 256), 256, 0, s>>>(idx.get(), n);
+        ST_LAUNCH("k_iota");
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) < (unsigned long long)T) ++bits;
+        size_t tmp = 0;
+        ST_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, lkey.get(), lkey2.get(), idx.get(), perm_out.get(),
+                                                (int)n, 0, bits, s));
+        DevArray<char> scratch(tmp, s);
+        ST_CUDA(cub::DeviceRadixSort::SortPairs(scratch.get(), tmp, lkey.get(), lkey2.get(), idx.get(),
+                                                perm_out.get(), (int)n, 0, bits, s));
+        perm = std::move(perm_out);
+        count_launch(2 + 3);
+    }
     mark("subtree+preorder");
     out.n = n;
     out.ncl = T;
