@@ -33,7 +33,6 @@ namespace {
 
 constexpr int kTile = 2048;      // elements per partition tile
 constexpr int kTileThreads = 256;
-constexpr int kGeomChunk = 4096; // elements per geometry work item
 
 __device__ __forceinline__ uint64_t ord_enc(double d) {
     const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
@@ -368,13 +367,33 @@ __global__ void k_compact(int C, int next_start, const int32_t* __restrict__ fla
     if (c < C && flag[c]) act[pos[c]] = next_start + c;
 }
 
+// subtree sizes, bottom-up one level per launch; with `mm`, also the tight boxes of the
+// level's internal clusters from their children's
 __global__ void k_subtree(int v0, int v1, const int32_t* __restrict__ first,
-                          const int32_t* __restrict__ nch, int32_t* __restrict__ size) {
+                          const int32_t* __restrict__ nch, int32_t* __restrict__ size,
+                          unsigned long long* __restrict__ mm) {
     const int v = v0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= v1) return;
     int s = 1;
-    for (int j = 0; j < nch[v]; ++j) s += size[first[v] + j];
+    const int k = nch[v];
+    for (int j = 0; j < k; ++j) s += size[first[v] + j];
     size[v] = s;
+    if (mm && k) {
+        uint64_t lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+        for (int j = 0; j < k; ++j) {
+            const unsigned long long* c = mm + 6 * (size_t)(first[v] + j);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = c[a] < lo[a] ? c[a] : lo[a];
+                hi[a] = hi[a] < c[3 + a] ? c[3 + a] : hi[a];
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mm[6 * (size_t)v + a] = lo[a];
+            mm[6 * (size_t)v + 3 + a] = hi[a];
+        }
+    }
 }
 
 __global__ void k_preorder(int v0, int v1, const int32_t* __restrict__ first,
@@ -387,57 +406,6 @@ __global__ void k_preorder(int v0, int v1, const int32_t* __restrict__ first,
     for (int j = 0; j < nch[v]; ++j) {
         pre[first[v] + j] = run;
         run += size[first[v] + j];
-    }
-}
-
-__global__ void k_nchunk(int T, const uint32_t* __restrict__ b, const uint32_t* __restrict__ e,
-                         int32_t* __restrict__ nck) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < T) nck[v] = (int32_t)((e[v] - b[v] + kGeomChunk - 1) / kGeomChunk);
-}
-
-__device__ __forceinline__ int find_item(const int32_t* __restrict__ off, int T, int item) {
-    int lo = 0, hi = T - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= item) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
-// Shrink: tight box of each cluster's range (cluster_tree.hpp:88), exact min/max.
-// `tpos`: positions in tree order (k_tree_pos), read contiguously per cluster range.
-__global__ void __launch_bounds__(256) k_minmax(int T, const int32_t* __restrict__ item_off,
-                                                const uint32_t* __restrict__ nb_begin,
-                                                const uint32_t* __restrict__ nb_end,
-                                                const double* __restrict__ tpos,
-                                                unsigned long long* __restrict__ mm) {
-    const int item = blockIdx.x;
-    const int v = find_item(item_off, T, item);
-    const uint32_t b = nb_begin[v] + (uint32_t)(item - item_off[v]) * kGeomChunk;
-    const uint32_t e = min(nb_end[v], b + kGeomChunk);
-    uint64_t lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
-    for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-        const double* p = tpos + 3 * (size_t)t;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const uint64_t q = ord_enc(p[a]);
-            lo[a] = q < lo[a] ? q : lo[a];
-            hi[a] = hi[a] < q ? q : hi[a];
-        }
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        lo[a] = warp_min(lo[a]);
-        hi[a] = warp_max(hi[a]);
-    }
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            atomicMin(&mm[6 * v + a], (unsigned long long)lo[a]);
-            atomicMax(&mm[6 * v + 3 + a], (unsigned long long)hi[a]);
-        }
     }
 }
 
@@ -454,30 +422,6 @@ __global__ void k_center(int T, int shrink, const unsigned long long* __restrict
         fbox[6 * v + 3 + a] = hi;
         center[3 * v + a] = __dmul_rn(__dadd_rn(lo, hi), 0.5);
     }
-}
-
-// radius^2 = max over the range of norm2(p - c) (cluster_tree.hpp:90-93); non-negative
-// doubles order like their bit patterns, so u64 atomicMax is exact.
-__global__ void __launch_bounds__(256) k_radius(int T, const int32_t* __restrict__ item_off,
-                                                const uint32_t* __restrict__ nb_begin,
-                                                const uint32_t* __restrict__ nb_end,
-                                                const double* __restrict__ tpos,
-                                                const double* __restrict__ center,
-                                                unsigned long long* __restrict__ r2max) {
-    const int item = blockIdx.x;
-    const int v = find_item(item_off, T, item);
-    const uint32_t b = nb_begin[v] + (uint32_t)(item - item_off[v]) * kGeomChunk;
-    const uint32_t e = min(nb_end[v], b + kGeomChunk);
-    const double c0 = center[3 * v], c1 = center[3 * v + 1], c2 = center[3 * v + 2];
-    uint64_t m = 0;
-    for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-        const double* p = tpos + 3 * (size_t)t;
-        const double r2 = norm2_rn(__dsub_rn(p[0], c0), __dsub_rn(p[1], c1), __dsub_rn(p[2], c2));
-        const uint64_t q = static_cast<uint64_t>(__double_as_longlong(r2));
-        m = m < q ? q : m;
-    }
-    m = warp_max(m);
-    if ((threadIdx.x & 31) == 0) atomicMax(&r2max[v], (unsigned long long)m);
 }
 
 // to_tree[perm[t]] = t
@@ -601,6 +545,106 @@ __global__ void k_leafkey(int T, const int32_t* __restrict__ nb_nch, const uint3
     for (uint32_t t = nb_begin[v] + (threadIdx.x & 31); t < nb_end[v]; t += 32) lkey[perm[t]] = key;
 }
 
+// ---- geometry ----
+// Tight boxes: one pass over the points for the leaves, then each level from its children
+// (min / max are exact and order-free, so a parent's box is its children's).  Points are
+// in tree order, so the lanes of a warp that share a leaf are consecutive: a segmented
+// reduction towards the run's first lane (shuffle down, kept while the neighbour is in the
+// same leaf) leaves one atomic per run.  Radii (which need every point again, against the
+// cluster's own centre) go by fixed-size chunks of each cluster's range.
+// leaf_of[t] = the leaf (BFS id) holding tree position t; one warp per cluster
+__global__ void k_leaf_of(int T, const int32_t* __restrict__ nb_nch, const uint32_t* __restrict__ nb_begin,
+                          const uint32_t* __restrict__ nb_end, int32_t* __restrict__ leaf_of) {
+    const int v = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+    if (v >= T || nb_nch[v] != 0) return;
+    for (uint32_t t = nb_begin[v] + (threadIdx.x & 31); t < nb_end[v]; t += 32) leaf_of[t] = v;
+}
+
+// segmented reduction over runs of equal `key` (consecutive lanes); returns true on a
+// run's first lane, which then holds the run's reduction
+template <class T, class Op>
+__device__ __forceinline__ bool seg_reduce(int key, T& v, Op op) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_down_sync(0xffffffffu, v, o);
+        const int k = __shfl_down_sync(0xffffffffu, key, o);
+        if (lane + o < 32 && k == key) v = op(v, y);
+    }
+    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    return lane == 0 || prev != key;
+}
+
+// tight boxes of the leaves (cluster_tree.hpp:88)
+__global__ void __launch_bounds__(256) k_leaf_minmax(uint32_t n, const double* __restrict__ tpos,
+                                                     const int32_t* __restrict__ leaf_of,
+                                                     unsigned long long* __restrict__ mm) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+    int v = -1;
+    if (t < n) {
+        v = leaf_of[t];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = ord_enc(tpos[3 * (size_t)t + a]);
+    }
+    auto mn = [](uint64_t x, uint64_t y) { return y < x ? y : x; };
+    auto mx = [](uint64_t x, uint64_t y) { return x < y ? y : x; };
+    bool head = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        head = seg_reduce(v, lo[a], mn);
+        seg_reduce(v, hi[a], mx);
+    }
+    if (head && v >= 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&mm[6 * v + a], (unsigned long long)lo[a]);
+            atomicMax(&mm[6 * v + 3 + a], (unsigned long long)hi[a]);
+        }
+    }
+}
+
+constexpr int kGeomChunk = 4096;  // points per radius work item
+
+__global__ void k_nchunk(int T, const uint32_t* __restrict__ b, const uint32_t* __restrict__ e,
+                         int32_t* __restrict__ nck) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < T) nck[v] = (int32_t)((e[v] - b[v] + kGeomChunk - 1) / kGeomChunk);
+}
+
+// radius^2 = max over the cluster of norm2(p - c) (cluster_tree.hpp:90-93); non-negative
+// doubles order like their bit patterns, so u64 atomicMax is exact.  One block per chunk of
+// a cluster's range; the grid is an upper bound of the chunk count (no host round trip),
+// blocks past item_off[T] exit.
+__global__ void __launch_bounds__(256) k_radius(int T, const int32_t* __restrict__ item_off,
+                                                const uint32_t* __restrict__ nb_begin,
+                                                const uint32_t* __restrict__ nb_end,
+                                                const double* __restrict__ tpos,
+                                                const double* __restrict__ center,
+                                                unsigned long long* __restrict__ r2max) {
+    const int item = blockIdx.x;
+    if (item >= item_off[T]) return;
+    int lo = 0, hi = T - 1;  // the cluster whose chunks hold `item`
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (item_off[mid] <= item) lo = mid;
+        else hi = mid - 1;
+    }
+    const int v = lo;
+    const uint32_t b = nb_begin[v] + (uint32_t)(item - item_off[v]) * kGeomChunk;
+    const uint32_t e = min(nb_end[v], b + kGeomChunk);
+    const double c0 = center[3 * v], c1 = center[3 * v + 1], c2 = center[3 * v + 2];
+    uint64_t m = 0;
+    for (uint32_t t = b + threadIdx.x; t < e; t += blockDim.x) {
+        const double* p = tpos + 3 * (size_t)t;
+        const double r2 = norm2_rn(__dsub_rn(p[0], c0), __dsub_rn(p[1], c1), __dsub_rn(p[2], c2));
+        const uint64_t q = static_cast<uint64_t>(__double_as_longlong(r2));
+        m = m < q ? q : m;
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomicMax(&r2max[v], (unsigned long long)m);
+}
+
 __global__ void k_iota(uint32_t* p, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = i;
@@ -621,13 +665,6 @@ void grow(DevArray<T>& a, size_t need, size_t used, cudaStream_t s) {
 }
 
 inline unsigned blocks(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
-
-int32_t read_i32(const int32_t* d, cudaStream_t s) {
-    int32_t h = 0;
-    ST_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
-    ST_CUDA(cudaStreamSynchronize(s));
-    return h;
-}
 
 }  // namespace
 
@@ -792,10 +829,36 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     const int T = total;
     const int L = (int)level_start.size() - 1;
 
+    // geometry, first half: positions in tree order (any order inside a leaf serves the
+    // order-free reductions, so this need not wait for the leaf sort below) and the
+    // leaves' tight boxes; the subtree pass folds them upwards
+    DevArray<double> tpos, center, fbox;
+    DevArray<unsigned long long> r2max, nmm;
+    if (geometry) {
+        tpos.alloc(3 * (size_t)n, s);
+        k_tree_pos<<<blocks(n, 256), 256, 0, s>>>(n, perm.get(), d_pos, tpos.get());
+        ST_LAUNCH("k_tree_pos");
+        count_launch();
+        if (shrink) {
+            DevArray<int32_t> leaf_of(n, s);
+            k_leaf_of<<<blocks((size_t)32 * T, 256), 256, 0, s>>>(T, nb_nch.get(), nb_begin.get(), nb_end.get(),
+                                                                  leaf_of.get());
+            ST_LAUNCH("k_leaf_of");
+            nmm.alloc(6 * (size_t)T, s);
+            // lo slots = +inf ordering (all ones), hi slots = 0
+            nmm.fill_bytes(0xff);
+            k_zero_hi<<<blocks(T, 256), 256, 0, s>>>(nmm.get(), T);
+            ST_LAUNCH("k_zero_hi");
+            k_leaf_minmax<<<blocks(n, 256), 256, 0, s>>>(n, tpos.get(), leaf_of.get(), nmm.get());
+            ST_LAUNCH("k_leaf_minmax");
+            count_launch(3);
+        }
+    }
+
     DevArray<int32_t> size(T, s), pre(T, s);
     for (int d = L - 1; d >= 0; --d) {
         const int v0 = level_start[d], v1 = level_start[d + 1];
-        k_subtree<<<blocks(v1 - v0, 128), 128, 0, s>>>(v0, v1, nb_first.get(), nb_nch.get(), size.get());
+        k_subtree<<<blocks(v1 - v0, 128), 128, 0, s>>>(v0, v1, nb_first.get(), nb_nch.get(), size.get(), nmm.get());
         ST_LAUNCH("k_subtree");
         count_launch();
     }
@@ -806,6 +869,30 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         ST_LAUNCH("k_preorder");
         count_launch();
     }
+    mark("subtree+preorder");
+
+    // geometry, second half: centres, then radii against them
+    if (geometry) {
+        center.alloc(3 * (size_t)T, s);
+        fbox.alloc(6 * (size_t)T, s);
+        r2max.alloc(T, s);
+        r2max.zero();
+        k_center<<<blocks(T, 128), 128, 0, s>>>(T, shrink ? 1 : 0, nmm.get(), nb_box.get(), fbox.get(),
+                                                center.get());
+        ST_LAUNCH("k_center");
+        DevArray<int32_t> nck(T, s), ioff(T + 1, s);
+        k_nchunk<<<blocks(T, 256), 256, 0, s>>>(T, nb_begin.get(), nb_end.get(), nck.get());
+        ST_LAUNCH("k_nchunk");
+        launch_scan_i32(nck.get(), ioff.get(), T, s);
+        // chunks <= sum over levels of (points / chunk + clusters of the level)
+        const size_t items_ub = (size_t)L * (n / kGeomChunk) + (size_t)T;
+        k_radius<<<(unsigned)items_ub, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), tpos.get(),
+                                                    center.get(), r2max.get());
+        ST_LAUNCH("k_radius");
+        count_launch(3);
+        tpos.reset();
+    }
+    mark("geometry");
 
     if (keyed) {
         // inside each leaf, input order (the reference's stable partitions): sort the points
@@ -831,7 +918,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         perm = std::move(perm_out);
         count_launch(2 + 3);
     }
-    mark("subtree+preorder");
+    mark("leaf order");
     out.n = n;
     out.ncl = T;
     out.depth = L - 1;
@@ -843,42 +930,6 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     out.bylevel.alloc(T, s);
     out.level_start = level_start;
 
-    DevArray<double> center, fbox;
-    DevArray<unsigned long long> r2max;
-    if (geometry) {
-        DevArray<int32_t> nck(T, s), ioff(T + 1, s);
-        k_nchunk<<<blocks(T, 256), 256, 0, s>>>(T, nb_begin.get(), nb_end.get(), nck.get());
-        ST_LAUNCH("k_nchunk");
-        launch_scan_i32(nck.get(), ioff.get(), T, s);
-        count_launch();
-        const int items = read_i32(ioff.get() + T, s);
-        DevArray<double> tpos(3 * (size_t)n, s);
-        k_tree_pos<<<blocks(n, 256), 256, 0, s>>>(n, perm.get(), d_pos, tpos.get());
-        ST_LAUNCH("k_tree_pos");
-        count_launch();
-        center.alloc(3 * (size_t)T, s);
-        fbox.alloc(6 * (size_t)T, s);
-        r2max.alloc(T, s);
-        r2max.zero();
-        DevArray<unsigned long long> nmm;
-        if (shrink) {
-            nmm.alloc(6 * (size_t)T, s);
-            // lo slots = +inf ordering (all ones), hi slots = 0
-            nmm.fill_bytes(0xff);
-            k_zero_hi<<<blocks(T, 256), 256, 0, s>>>(nmm.get(), T);
-            ST_LAUNCH("k_zero_hi");
-            k_minmax<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), tpos.get(), nmm.get());
-            ST_LAUNCH("k_minmax");
-            count_launch(2);
-        }
-        k_center<<<blocks(T, 128), 128, 0, s>>>(T, shrink ? 1 : 0, nmm.get(), nb_box.get(), fbox.get(),
-                                                center.get());
-        ST_LAUNCH("k_center");
-        k_radius<<<items, 256, 0, s>>>(T, ioff.get(), nb_begin.get(), nb_end.get(), tpos.get(), center.get(),
-                                       r2max.get());
-        ST_LAUNCH("k_radius");
-        count_launch(2);
-    }
     k_finalize<<<blocks(T, 128), 128, 0, s>>>(T, geometry ? 1 : 0, pre.get(), size.get(), nb_begin.get(),
                                               nb_end.get(), nb_first.get(), nb_nch.get(), center.get(),
                                               r2max.get(), fbox.get(), out.geom.get(), out.info.get(),
@@ -891,7 +942,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     ST_LAUNCH("k_invperm");
     count_launch();
     out.perm = std::move(perm);
-    mark("geometry+finalize");
+    mark("finalize");
     if (dbg) {
         ST_CUDA(cudaStreamSynchronize(s));
         std::string line = "[build] n " + std::to_string(n) + " levels " + std::to_string(depth) + ":";
