@@ -474,25 +474,20 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     const int P = prm.order + (str ? 2 : 1);
 
     if (nshards > 1) {
-        // work-balanced contiguous warp ranges, identical on every rank (deterministic)
-        DevArray<float> cost(nwarps, s);
-        a.warp_cost = cost.get();
-        // a dense far event costs ~8 (P+1)^2 warp DP instructions; a near (lane, source)
-        // pair ~1 (30 per 32 lanes)
-        a.sparse_max = far_sparse_max();
-        const float cf = (float)((P + 1) * (P + 1) * 8), cn = 1.f;
-        launch_count(a, cf, cn, s);
-        std::vector<float> hc(nwarps);
-        ST_CUDA(cudaMemcpyAsync(hc.data(), cost.get(), sizeof(float) * nwarps, cudaMemcpyDeviceToHost, s));
-        ST_CUDA(cudaStreamSynchronize(s));
+        // work-balanced contiguous warp ranges, identical on every rank (deterministic):
+        // sampled counting walk and the cut on the device, two integers back to the host
         const int stride = count_stride(nwarps);
-        for (int w = 0; w < nwarps; ++w)  // every stride-th warp was sampled
-            if (w % stride) hc[w] = hc[w - w % stride];
-        std::vector<double> w(hc.begin(), hc.end());
-        std::vector<size_t> cuts(nshards + 1);
-        shard_cuts_host(nwarps, w.data(), nshards, cuts.data());
-        a.w0 = (int)cuts[shard];
-        a.w1 = (int)cuts[shard + 1];
+        DevArray<unsigned long long> cost((nwarps + stride - 1) / stride, s);
+        DevArray<int> dcuts(nshards + 1, s);
+        a.warp_cost = cost.get();
+        a.sparse_max = far_sparse_max();
+        launch_count(a, (uint32_t)((P + 1) * (P + 1) * 8), s);
+        launch_shard_cuts(cost.get(), nwarps, stride, nshards, dcuts.get(), s);
+        int wr[2] = {0, 0};
+        ST_CUDA(cudaMemcpyAsync(wr, dcuts.get() + shard, sizeof wr, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        a.w0 = wr[0];
+        a.w1 = wr[1];
         a.warp_cost = nullptr;
     }
     ec.record(s);
@@ -625,8 +620,10 @@ void shard_cuts_impl(size_t n, const double* w, int k, size_t* cuts) {
     double run = 0.0;
     size_t i = 0;
     for (int sIdx = 1; sIdx < k; ++sIdx) {
-        const double target = total * sIdx / k;
-        while (i < n && run + 0.5 * (w[i] > 0 ? w[i] : 0.0) < target) {
+        // run + w/2 < total s / k, multiplied out (exact for integer weights below 2^48,
+        // the form k_shard_cuts evaluates in integers)
+        const double target = 2.0 * total * sIdx;
+        while (i < n && 2.0 * k * run + k * (w[i] > 0 ? w[i] : 0.0) < target) {
             run += w[i] > 0 ? w[i] : 0.0;
             ++i;
         }

@@ -26,7 +26,7 @@ struct TravArgs {
     uint64_t* per_target = nullptr;  // optional {visited, far, direct}, original order
     unsigned long long* stats = nullptr;  // {farfield_evals, direct_pairs, clusters_visited}
     int* err = nullptr;              // set to 1 on a coincident source/target pair
-    float* warp_cost = nullptr;      // count pass: per-warp work estimate
+    unsigned long long* warp_cost = nullptr;  // count pass: sampled warps' work estimates (integer)
     int out_batch = 0;               // 1: write out / per_target in batch order (slot t), not torig[t]
     int* work = nullptr;             // persistent kernels: next batch counter (zeroed per launch)
     // far events accepted by <= sparse_max lanes of a warp are evaluated by the packed
@@ -67,8 +67,12 @@ void launch_eval(bool sto, bool str, const TravArgs& a, const FarOrder* orders, 
 // Interaction lists (pre-order cluster ids, DFS order) of the targets in a.tx.
 void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64_t* nfar, int64_t* nnear,
                   cudaStream_t s);
-// Traversal-only work estimate of every 4th warp of [a.w0, a.w1) into a.warp_cost (for
-// multi-GPU shard cuts; the caller fills the warps in between from the preceding sample).
+// Traversal-only work estimate of every count_stride(w)-th warp of [a.w0, a.w1) into
+// a.warp_cost[(warp - w0) / stride] (for multi-GPU shard cuts; each sample stands for the
+// stride warps from it).  Integer units: a dense far event costs 24 x 8 (P+1)^2 (~its warp DP
+// instructions), a sparse one (na lanes) 8 (P+1)^2 na (its packed share), a near (lane,
+// source) pair 24.  Integers make every prefix sum exact, so the cut is the same however it
+// is summed.
 constexpr int kCountStride = 4;
 // every count_stride(w)-th of w batch warps is walked for the shard cuts: at least every
 // 4th, at most ~8K samples (the per-warp cost is smooth along the Morton order)
@@ -84,7 +88,13 @@ inline int count_samples() {
 inline int count_stride(int warps) {
     return warps / count_samples() > kCountStride ? warps / count_samples() : kCountStride;
 }
-void launch_count(const TravArgs& a, float far_cost, float near_cost, cudaStream_t s);
+void launch_count(const TravArgs& a, uint32_t far_cost, cudaStream_t s);
+// Work-balanced contiguous cuts of the warps [0, nwarps) into k shards from the samples
+// (sample g = warps [g stride, min((g+1) stride, nwarps))), on the device: cut s is the
+// first warp i with prefix(i) + w(i) / 2 >= s total / k (shard_cuts_host's rule, in exact
+// integers).  cuts[0..k] (int32).
+void launch_shard_cuts(const unsigned long long* samples, int nwarps, int stride, int k, int* cuts,
+                       cudaStream_t s);
 
 // O(N^2) contracted direct sum (kernels.hpp:45-83, 123-150): sources are the
 // original-order records [n][12]; targets are source indices (self skipped).

@@ -3,12 +3,12 @@
 * batch order: 63-bit Morton keys of the targets in their tight box, stably sorted
   (csrc/tree.cu order_targets / k_morton: 21 bits per axis, x in the top bit of each
   triple; CUB radix sort on the keys, original index as the tie order);
-* per-warp cost of the shard cuts: csrc/traverse.cu k_count in float32, summed in
-  cluster pre-order (the order the warp's stackless walk meets the clusters): an accepted
-  cluster costs cf = 8 (P+1)^2 when more than `sparse_max` lanes accept it, cf * lanes / 24
-  otherwise; a near leaf costs lanes * leaf size; every stride-th warp is walked and the
-  others take the preceding sample's cost (capi.cu run_treecode);
-* cuts: st_shard_cuts (the library's host function) on those costs.
+* per-warp cost of the shard cuts: csrc/traverse.cu k_count in exact integers: an
+  accepted cluster costs 24 cf, cf = 8 (P+1)^2, when more than `sparse_max` lanes accept
+  it, cf * lanes otherwise; a near leaf costs 24 * lanes * leaf size; every stride-th warp
+  is walked and the others take the preceding sample's cost;
+* cuts: st_shard_cuts (the library's host function) on those costs -- the same rule that
+  k_shard_cuts evaluates on the device (capi.cu run_treecode).
 
 tests/test_multirank.py shards with it on CPU (gloo); tests/test_gpu_parity.py checks it
 against the library's own batch order and shard ranges on a GPU."""
@@ -47,13 +47,15 @@ def count_stride(warps):
 
 def warp_costs(order, far_lists, near_lists, leaf_size, P, sparse_max=SPARSE_MAX):
     """k_count's per-warp cost for the batch order `order` (per-target far / near lists in
-    original target order; leaf_size[c] = end - begin of cluster c)."""
-    f32 = np.float32
+    original target order; leaf_size[c] = end - begin of cluster c), in its integer units:
+    a dense far event 24 x 8 (P+1)^2, a sparse one 8 (P+1)^2 x its lanes, a near (lane,
+    source) pair 24.  Every count_stride-th warp is sampled; the warps after a sample
+    take its cost."""
     nt = len(order)
     nw = (nt + 31) // 32
-    cf, cn = f32((P + 1) * (P + 1) * 8), f32(1.0)
+    cf = (P + 1) * (P + 1) * 8
     stride = count_stride(nw)
-    cost = np.zeros(nw, np.float32)
+    cost = np.zeros(nw, np.int64)
     for w in range(0, nw, stride):
         nacc, nleaf = {}, {}
         for t in order[32 * w:32 * w + 32]:
@@ -61,13 +63,13 @@ def warp_costs(order, far_lists, near_lists, leaf_size, P, sparse_max=SPARSE_MAX
                 nacc[int(c)] = nacc.get(int(c), 0) + 1
             for c in near_lists[t]:
                 nleaf[int(c)] = nleaf.get(int(c), 0) + 1
-        acc = f32(0.0)
-        for c in sorted(set(nacc) | set(nleaf)):
+        acc = 0
+        for c in set(nacc) | set(nleaf):
             na, nl = nacc.get(c, 0), nleaf.get(c, 0)
             if na:
-                acc = f32(acc + (cf if na > sparse_max else f32(f32(cf * f32(na)) / f32(24.0))))
+                acc += 24 * cf if na > sparse_max else cf * na
             if nl:
-                acc = f32(acc + f32(cn * f32(nl)) * f32(leaf_size[c]))
+                acc += 24 * nl * int(leaf_size[c])
         cost[w] = acc
     for w in range(nw):
         if w % stride:
