@@ -393,20 +393,21 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     if (nt >= 0x7fffffffull - 64) fail(ST_INVALID_ARGUMENT, "too many targets");
     Event e0, e1, e2, e3;
     e0.record(s);
-    // Second stream: the targets' Morton order (positions only) overlaps the tree build's
-    // host-synchronised levels; then K2 (below).  Declared before every array whose
-    // stream-ordered free goes to it.
+    // Second stream: the batch order of disjoint targets (positions only) overlaps the tree
+    // build; then K2 (below).  Declared before every array whose stream-ordered free goes
+    // to it.  Targets that are the sources take the build's own key order.
     AuxStream aux;
     ST_CUDA(cudaStreamWaitEvent(aux.s, e0.e, 0));
     const double* tpos = same ? src.pos : d_targets;
     DevArray<uint32_t> tperm;
-    order_targets(tpos, nt, aux.s, tperm);
+    if (!same) order_targets(tpos, nt, aux.s, tperm);
     Event esort;
     esort.record(aux.s);
 
     // K1: tree over the sources, tree-ordered source records
     DevTree tree;
-    build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree, same ? &tperm : nullptr);
+    if (same && tperm.size() != nt) order_targets(tpos, nt, s, tperm);  // the build made no key order
     const MomentsPlan mplan = plan_moments(tree, s);  // host lists now: K2 below never waits on the host
     // Validation and the tree-ordered source records on the second stream: only the near
     // field (and the moments after them there) read the records, so they overlap the
@@ -435,8 +436,8 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     Event erec;
     erec.record(aux.s);
 
-    // batch order of the targets: 63-bit Morton order in their tight box (one radix sort,
-    // done on the second stream above)
+    // batch order of the targets: their 30-bit octree-key order (one radix sort, from the
+    // build or on the second stream above)
     ST_CUDA(cudaStreamWaitEvent(s, esort.e, 0));
     DevArray<double> tx(3 * nt, s), ufar(3 * nt, s);
     DevArray<uint32_t> torig(nt, s), tskip(nt, s);
@@ -648,7 +649,8 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     Event e0, e1, e2, e3;
     e0.record(s);
     DevTree tree;
-    build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree);
+    DevArray<uint32_t> tperm;
+    build_tree_device(src.pos, n, prm.leaf_capacity, prm.shrink != 0, true, s, tree, same ? &tperm : nullptr);
     const MomentsPlan mplan = plan_moments(tree, s);
     DevArray<unsigned long long> vflags(6, s);
     vflags.fill_bytes(0xff);
@@ -675,8 +677,7 @@ void run_sweep(const DevParticles& src, const double* d_targets, size_t nt_in, c
     DevArray<double> M;
     compute_moments_device(tree, rec.get(), pmax, sto, str, aux.s, M, &mplan);
     const double* tpos = same ? src.pos : d_targets;
-    DevArray<uint32_t> tperm;
-    order_targets(tpos, nt, s, tperm);
+    if (tperm.size() != nt) order_targets(tpos, nt, s, tperm);
     DevArray<double> tx(3 * nt, s);
     DevArray<uint32_t> torig(nt, s), tskip(nt, s);
     k_targets<<<nblocks(nt, 256), 256, 0, s>>>(nt, tperm.get(), tpos, same ? to_tree.get() : nullptr, tx.get(),
@@ -795,7 +796,7 @@ int peer_exchange(void* vctx, const st_shard_exchange* ex) {
 
 // Replicated-data multi-GPU in one process (PAPER.md:986-1030 with GPUs for MPI ranks):
 // one host thread per logical device uploads the inputs, rebuilds the (bit-identical)
-// tree and moments and evaluates its work-balanced shard of the Morton-ordered batches.
+// tree and moments and evaluates its work-balanced shard of the key-ordered batches.
 // The shard's epilogue (k_nreduce, and the count walk for per-target statistics) stores
 // straight into device 0's output in original order -- NVLink peer stores from the
 // kernel, no gather or scatter pass.  Logical devices beyond the physical count share

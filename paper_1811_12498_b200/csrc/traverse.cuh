@@ -12,7 +12,7 @@ namespace st {
 constexpr uint32_t kNoSkip = 0xffffffffu;
 
 struct TravArgs {
-    const double* tx = nullptr;      // targets in batch (Morton) order, xyz
+    const double* tx = nullptr;      // targets in batch (octree-key) order, xyz
     const uint32_t* tskip = nullptr; // source tree index excluded per target (kNoSkip: none)
     const uint32_t* torig = nullptr; // original target index per batch position
     int nt = 0;
@@ -75,7 +75,7 @@ void launch_lists(const TravArgs& a, int cap, int32_t* far, int32_t* near, int64
 // is summed.
 constexpr int kCountStride = 4;
 // every count_stride(w)-th of w batch warps is walked for the shard cuts: at least every
-// 4th, at most ~8K samples (the per-warp cost is smooth along the Morton order)
+// 4th, at most ~8K samples (the per-warp cost is smooth along the key order)
 // ST_COUNT_SAMPLES overrides the ~8K sampled warps (A/B of the multi-GPU cut cost).
 inline int count_samples() {
     static const int v = [] {

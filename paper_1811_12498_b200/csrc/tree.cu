@@ -17,6 +17,7 @@
 // Geometry uses the reference's exact non-FMA expressions (__dadd_rn /
 // __dmul_rn), and min / max / max-of-norm2 are order-free exact reductions.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <string>
 #include <utility>
@@ -25,7 +26,10 @@
 #include "scan.cuh"
 #include "tree.cuh"
 
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
+
+namespace cg = cooperative_groups;
 
 namespace st {
 
@@ -104,36 +108,6 @@ __global__ void k_tight_all(const double* __restrict__ pos, size_t n,
         atomicMin(&mm[a], (unsigned long long)l);
         atomicMax(&mm[3 + a], (unsigned long long)h);
     }
-}
-
-// 63-bit Morton key (21 bits per axis) of each point inside the tight box: the order of
-// the target batches (any spatially coherent order serves; results do not depend on it)
-__device__ __forceinline__ uint64_t spread21(uint64_t v) {
-    v &= 0x1fffffull;
-    v = (v | v << 32) & 0x1f00000000ffffull;
-    v = (v | v << 16) & 0x1f0000ff0000ffull;
-    v = (v | v << 8) & 0x100f00f00f00f00full;
-    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
-    v = (v | v << 2) & 0x1249249249249249ull;
-    return v;
-}
-__global__ void k_morton(const double* __restrict__ pos, size_t n, const unsigned long long* __restrict__ mm,
-                         uint64_t* __restrict__ key, uint32_t* __restrict__ idx) {
-    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double lo[3], side = 0.0;
-    for (int a = 0; a < 3; ++a) {
-        lo[a] = ord_dec(mm[a]);
-        side = fmax(side, ord_dec(mm[3 + a]) - lo[a]);
-    }
-    const double inv = side > 0.0 ? 2097151.0 / side : 0.0;
-    uint64_t k = 0;
-    for (int a = 0; a < 3; ++a) {
-        const double q = fmin(fmax((pos[3 * i + a] - lo[a]) * inv, 0.0), 2097151.0);
-        k |= spread21((uint64_t)q) << (2 - a);
-    }
-    key[i] = k;
-    idx[i] = (uint32_t)i;
 }
 
 // Root cube (cluster_tree.hpp:163-169): side = max extent * (1 + 1e-12), centred
@@ -534,6 +508,153 @@ __global__ void k_split_sorted(int m, int d, const int32_t* __restrict__ act, co
     if (k == 0) seg_begin[s] = b;
 }
 
+// All keyed levels in one cooperative launch (no host round trip per level).  Every block
+// walks the levels in lockstep, grid-wide barriers between the phases of a level:
+//   A  8 threads per active segment binary-search its children's ranges (k_split_sorted)
+//   B  block 0: child counts -> exclusive scan over the segments (chbase), C
+//   C  children records and next-level flags (k_children)
+//   D  block 0: scan of the flags -> next active list, level bookkeeping
+// Sizes are bounded up front: an active segment holds more than n0 points, so a level has
+// at most mcap = n / (n0 + 1) of them and at most 8 mcap children.
+struct KeyedLevels {
+    int n0 = 0;
+    int mcap = 0, tcap = 0;
+    const uint32_t* skey = nullptr;
+    uint32_t* nb_begin = nullptr;
+    uint32_t* nb_end = nullptr;
+    double* nb_box = nullptr;
+    int32_t* nb_first = nullptr;
+    int32_t* nb_nch = nullptr;
+    int32_t* act[2] = {nullptr, nullptr};  // ping-pong active lists [mcap]
+    uint32_t* seg_cnt = nullptr;           // [8 mcap]
+    int32_t* chbase = nullptr;             // [mcap + 1]
+    int32_t* flag = nullptr;               // [8 mcap + 1] (exclusive scan in place)
+    int32_t* state = nullptr;              // m, total, depth, which act, overflow, level_start[kKeyLevels + 2]
+};
+constexpr int kKeyThreads = 512;
+enum { KS_M = 0, KS_TOTAL, KS_DEPTH, KS_ACT, KS_OVER, KS_LS };
+
+// block-wide exclusive scan of int32 values in place over [0, cnt); returns the total
+__device__ int block_scan_inplace(int32_t* a, int cnt, int32_t* sh) {
+    const int per = (cnt + kKeyThreads - 1) / kKeyThreads;
+    const int i0 = min(cnt, (int)threadIdx.x * per), i1 = min(cnt, i0 + per);
+    int sum = 0;
+    for (int i = i0; i < i1; ++i) sum += a[i];
+    sh[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < kKeyThreads; o <<= 1) {
+        const int y = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += y;
+        __syncthreads();
+    }
+    int run = sh[threadIdx.x] - sum;
+    for (int i = i0; i < i1; ++i) {
+        const int x = a[i];
+        a[i] = run;
+        run += x;
+    }
+    const int total = sh[kKeyThreads - 1];
+    __syncthreads();
+    return total;
+}
+
+__global__ void __launch_bounds__(kKeyThreads) k_keyed_levels(const KeyedLevels K) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t sh[kKeyThreads];
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
+    for (;;) {
+        const int m = *(volatile int32_t*)&K.state[KS_M];
+        const int depth = *(volatile int32_t*)&K.state[KS_DEPTH];
+        const int total = *(volatile int32_t*)&K.state[KS_TOTAL];
+        const int32_t* act = K.act[*(volatile int32_t*)&K.state[KS_ACT]];
+        int32_t* act2 = K.act[1 - *(volatile int32_t*)&K.state[KS_ACT]];
+        if (m == 0 || depth >= kKeyLevels || K.state[KS_OVER]) break;
+        // A: child ranges
+        const int sh3 = 3 * (kKeyLevels - 1 - depth);
+        for (int g = gtid; g < 8 * m; g += gsz) {
+            const int sg = g >> 3, k = g & 7;
+            const int v = act[sg];
+            uint32_t lo = K.nb_begin[v], hi = K.nb_end[v];
+            while (lo < hi) {
+                const uint32_t mid = lo + ((hi - lo) >> 1);
+                if ((int)((K.skey[mid] >> sh3) & 7u) < k) lo = mid + 1;
+                else hi = mid;
+            }
+            K.seg_cnt[g] = lo;  // start of slot k; counts in B
+        }
+        grid.sync();
+        // B: counts, children per segment, exclusive scan
+        if (blockIdx.x == 0) {
+            for (int sg = threadIdx.x; sg < m; sg += blockDim.x) {
+                const uint32_t e = K.nb_end[act[sg]];
+                int c = 0;
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t st = K.seg_cnt[8 * sg + k], en = k == 7 ? e : K.seg_cnt[8 * sg + k + 1];
+                    c += en > st;
+                }
+                K.chbase[sg] = c;
+            }
+            __syncthreads();
+            const int C = block_scan_inplace(K.chbase, m, sh);
+            if (threadIdx.x == 0) {
+                K.chbase[m] = C;
+                if (total + C > K.tcap || C > 8 * K.mcap) K.state[KS_OVER] = 1;
+            }
+        }
+        grid.sync();
+        if (K.state[KS_OVER]) break;
+        const int C = K.chbase[m];
+        // C: children records (cluster_tree.hpp:125-137), flags of the next level's splits
+        for (int sg = gtid; sg < m; sg += gsz) {
+            const int v = act[sg];
+            double glo[3], ghi[3], mid[3];
+            for (int a = 0; a < 3; ++a) {
+                glo[a] = K.nb_box[6 * v + a];
+                ghi[a] = K.nb_box[6 * v + 3 + a];
+                mid[a] = __dmul_rn(__dadd_rn(glo[a], ghi[a]), 0.5);
+            }
+            const uint32_t e = K.nb_end[v];
+            int c = total + K.chbase[sg];
+            K.nb_first[v] = c;
+            K.nb_nch[v] = K.chbase[sg + 1] - K.chbase[sg];
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t st = K.seg_cnt[8 * sg + k], en = k == 7 ? e : K.seg_cnt[8 * sg + k + 1];
+                if (en <= st) continue;
+                for (int a = 0; a < 3; ++a) {
+                    const bool up = (k >> a) & 1;
+                    K.nb_box[6 * c + a] = up ? mid[a] : glo[a];
+                    K.nb_box[6 * c + 3 + a] = up ? ghi[a] : mid[a];
+                }
+                K.nb_begin[c] = st;
+                K.nb_end[c] = en;
+                K.nb_first[c] = -1;
+                K.nb_nch[c] = 0;
+                // cluster_tree.hpp:96: leaf iff count <= N0 or depth >= 64
+                K.flag[c - total] = (en - st > (uint32_t)K.n0 && depth + 1 < 64) ? 1 : 0;
+                ++c;
+            }
+        }
+        grid.sync();
+        // D: next active list
+        if (blockIdx.x == 0) {
+            const int m2 = block_scan_inplace(K.flag, C, sh);
+            for (int c = threadIdx.x; c < C; c += blockDim.x) {
+                const int next = c + 1 < C ? K.flag[c + 1] : m2;
+                if (next > K.flag[c]) act2[K.flag[c]] = total + c;
+            }
+            if (threadIdx.x == 0) {
+                K.state[KS_LS + depth + 1] = total;
+                K.state[KS_TOTAL] = total + C;
+                K.state[KS_DEPTH] = depth + 1;
+                K.state[KS_M] = m2;
+                K.state[KS_ACT] = 1 - K.state[KS_ACT];
+            }
+        }
+        grid.sync();
+    }
+}
+
 // Leaf key of every point: the leaf's pre-order id (leaves in pre-order = tree order),
 // stored at the point's input index.  One warp per cluster; internal clusters skip.
 __global__ void k_leafkey(int T, const int32_t* __restrict__ nb_nch, const uint32_t* __restrict__ nb_begin,
@@ -669,7 +790,7 @@ inline unsigned blocks(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bool geometry,
-                       cudaStream_t s, DevTree& out) {
+                       cudaStream_t s, DevTree& out, DevArray<uint32_t>* key_order) {
     if (n_sz == 0) fail(ST_INVALID_ARGUMENT, "build_tree: empty particle set");
     if (n0 < 1) fail(ST_INVALID_ARGUMENT, "build_tree: leaf capacity must be >= 1");
     if (n_sz >= 0x7fffffffull) fail(ST_INVALID_ARGUMENT, "build_tree: more than 2^31-1 particles");
@@ -678,10 +799,13 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     // ST_DEBUG_BUILD=1: device-time marks of the build's phases (stderr)
     static const bool dbg = getenv("ST_DEBUG_BUILD") != nullptr;
     std::vector<std::pair<const char*, Event>> marks;
+    std::vector<double> host_ms;  // host clock at each mark (is the GPU waiting for the host?)
+    const auto h0 = std::chrono::steady_clock::now();
     auto mark = [&](const char* what) {
         if (!dbg) return;
         marks.emplace_back(what, Event());
         marks.back().second.record(s);
+        host_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
     };
     mark("start");
 
@@ -740,6 +864,69 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
     DevArray<int32_t> act(std::max(m, 1), s);
     if (m) ST_CUDA(cudaMemsetAsync(act.get(), 0, sizeof(int32_t), s));
     int depth = 0;
+    bool deep = false;
+
+    // the keyed levels in one cooperative launch when their sizes are bounded (mcap: at most
+    // n / (n0 + 1) splitting segments per level); ST_TREE_LEVEL_LOOP=1 keeps the per-level
+    // host loop below
+    static const bool level_loop = getenv("ST_TREE_LEVEL_LOOP") != nullptr;
+    const long long mcap_ll = (long long)n / ((long long)n0 + 1) + 1;
+    if (keyed && m && !level_loop && mcap_ll <= 65536) {
+        const int mcap = (int)mcap_ll;
+        const int tcap = 1 + 8 * kKeyLevels * mcap;
+        grow(nb_begin, tcap, total, s);
+        grow(nb_end, tcap, total, s);
+        grow(nb_first, tcap, total, s);
+        grow(nb_nch, tcap, total, s);
+        grow(nb_box, 6 * (size_t)tcap, 6 * (size_t)total, s);
+        DevArray<int32_t> actb[2] = {DevArray<int32_t>(mcap, s), DevArray<int32_t>(mcap, s)};
+        DevArray<uint32_t> kseg((size_t)8 * mcap, s);
+        DevArray<int32_t> kch(mcap + 1, s), kflag((size_t)8 * mcap + 1, s), kst(KS_LS + kKeyLevels + 2, s);
+        int32_t st0[KS_LS + kKeyLevels + 2] = {};
+        st0[KS_M] = 1;
+        st0[KS_TOTAL] = 1;
+        ST_CUDA(cudaMemcpyAsync(kst.get(), st0, sizeof st0, cudaMemcpyHostToDevice, s));
+        ST_CUDA(cudaMemsetAsync(actb[0].get(), 0, sizeof(int32_t), s));
+        KeyedLevels K;
+        K.n0 = n0;
+        K.mcap = mcap;
+        K.tcap = tcap;
+        K.skey = skey.get();
+        K.nb_begin = nb_begin.get();
+        K.nb_end = nb_end.get();
+        K.nb_box = nb_box.get();
+        K.nb_first = nb_first.get();
+        K.nb_nch = nb_nch.get();
+        K.act[0] = actb[0].get();
+        K.act[1] = actb[1].get();
+        K.seg_cnt = kseg.get();
+        K.chbase = kch.get();
+        K.flag = kflag.get();
+        K.state = kst.get();
+        static int grid = [] {
+            int dev = 0, sms = 0, per = 0;
+            ST_CUDA(cudaGetDevice(&dev));
+            ST_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            ST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_keyed_levels, kKeyThreads, 0));
+            return std::max(1, std::min(sms, sms * per));
+        }();
+        void* args[] = {&K};
+        ST_CUDA(cudaLaunchCooperativeKernel((const void*)k_keyed_levels, grid, kKeyThreads, args, 0, s));
+        ST_LAUNCH("k_keyed_levels");
+        count_launch();
+        ST_CUDA(cudaMemcpyAsync(st0, kst.get(), sizeof st0, cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        if (st0[KS_OVER]) fail(ST_RUNTIME_ERROR, "build_tree: keyed levels exceeded their bound");
+        depth = st0[KS_DEPTH];
+        for (int d = 1; d <= depth; ++d) level_start.push_back(st0[KS_LS + d]);
+        total = st0[KS_TOTAL];
+        m = st0[KS_M];
+        act = DevArray<int32_t>(std::max(m, 1), s);
+        if (m)
+            ST_CUDA(cudaMemcpyAsync(act.get(), actb[st0[KS_ACT]].get(), sizeof(int32_t) * m, cudaMemcpyDeviceToDevice,
+                                    s));
+        mark("keyed levels");
+    }
 
     while (m > 0) {
         DevArray<uint32_t> seg_begin(m, s), seg_end, seg_base, seg_cnt((size_t)8 * m, s);
@@ -753,6 +940,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
             ST_LAUNCH("k_split_sorted");
             count_launch();
         } else {
+            deep = true;  // perm is no longer the plain key order
             if (!seg_of.size()) {
                 skey.reset();
                 seg_of.alloc(n, s);
@@ -915,6 +1103,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         DevArray<char> scratch(tmp, s);
         ST_CUDA(cub::DeviceRadixSort::SortPairs(scratch.get(), tmp, lkey.get(), lkey2.get(), idx.get(),
                                                 perm_out.get(), (int)n, 0, bits, s));
+        if (key_order && !deep) *key_order = std::move(perm);
         perm = std::move(perm_out);
         count_launch(2 + 3);
     }
@@ -949,8 +1138,8 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         for (size_t i = 1; i < marks.size(); ++i) {
             float ms = 0.f;
             ST_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].second.e, marks[i].second.e));
-            char buf[64];
-            snprintf(buf, sizeof buf, " %s %.3f", marks[i].first, ms);
+            char buf[96];
+            snprintf(buf, sizeof buf, " %s %.3f (host %.3f)", marks[i].first, ms, host_ms[i] - host_ms[i - 1]);
             line += buf;
         }
         fprintf(stderr, "%s ms\n", line.c_str());
@@ -963,20 +1152,23 @@ void order_targets(const double* d_pos, size_t n, cudaStream_t s, DevArray<uint3
     DevArray<unsigned long long> mm(6, s);
     const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
     ST_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof init, cudaMemcpyHostToDevice, s));
-    const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
+    const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 8);
     k_tight_all<<<g, 256, 0, s>>>(d_pos, n, mm.get());
     ST_LAUNCH("k_tight_all");
-    DevArray<uint64_t> key(n, s), key2(n, s);
-    DevArray<uint32_t> idx(n, s);
-    k_morton<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d_pos, n, mm.get(), key.get(), idx.get());
-    ST_LAUNCH("k_morton");
+    DevArray<uint32_t> rng(2, s);
+    DevArray<double> box(6, s);
+    k_root<<<1, 1, 0, s>>>(mm.get(), (uint32_t)n, rng.get(), rng.get() + 1, box.get());
+    ST_LAUNCH("k_root");
+    DevArray<uint32_t> key(n, s), key2(n, s), idx(n, s);
+    k_geokey<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((uint32_t)n, d_pos, box.get(), key.get(), idx.get());
+    ST_LAUNCH("k_geokey");
     size_t tmp = 0;
     ST_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), key2.get(), idx.get(), perm.get(), (int)n, 0,
-                                            63, s));
+                                            3 * kKeyLevels, s));
     DevArray<char> scratch(tmp, s);
     ST_CUDA(cub::DeviceRadixSort::SortPairs(scratch.get(), tmp, key.get(), key2.get(), idx.get(), perm.get(), (int)n,
-                                            0, 63, s));
-    count_launch(3);
+                                            0, 3 * kKeyLevels, s));
+    count_launch(3 + 5);
 }
 
 }  // namespace st

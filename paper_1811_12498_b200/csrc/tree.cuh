@@ -25,11 +25,15 @@ struct DevTree {
 
 // Builds the tree of n points (xyz interleaved, device) with leaf capacity n0.
 // geometry=false skips bbox/center/radius (used for the target ordering tree).
+// key_order (optional): the points' octree-key order (below), when the build made it on the
+// way (left empty otherwise) -- the batch order of the same points as targets.
 void build_tree_device(const double* d_pos, size_t n, int n0, bool shrink, bool geometry,
-                       cudaStream_t s, DevTree& out);
+                       cudaStream_t s, DevTree& out, DevArray<uint32_t>* key_order = nullptr);
 
-// Order of n points (device, xyz) by 63-bit Morton key in their tight box: perm[i] is the
-// original index of the i-th point.  Stream-ordered, no host synchronisation.
+// Batch order of n points (device, xyz): stable order of their 30-bit octree keys (ten
+// levels of bisection of the root cube of their tight box, cluster_tree.hpp:163-169, the
+// tree build's own first levels); perm[i] is the original index of the i-th point.
+// Stream-ordered, no host synchronisation.
 void order_targets(const double* d_pos, size_t n, cudaStream_t s, DevArray<uint32_t>& perm);
 
 }  // namespace st

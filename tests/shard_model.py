@@ -1,8 +1,9 @@
 """Host restatement of the multi-GPU planning of the CUDA path (test infrastructure).
 
-* batch order: 63-bit Morton keys of the targets in their tight box, stably sorted
-  (csrc/tree.cu order_targets / k_morton: 21 bits per axis, x in the top bit of each
-  triple; CUB radix sort on the keys, original index as the tie order);
+* batch order: 30-bit octree keys of the targets (ten levels of bisection of the root
+  cube of their tight box, x in the low bit of each level's digit), stably sorted
+  (csrc/tree.cu order_targets / k_geokey and the tree build's own key sort; CUB radix
+  sort on the keys, original index as the tie order);
 * per-warp cost of the shard cuts: csrc/traverse.cu k_count in exact integers: an
   accepted cluster costs 24 cf, cf = 8 (P+1)^2, when more than `sparse_max` lanes accept
   it, cf * lanes otherwise; a near leaf costs 24 * lanes * leaf size; every stride-th warp
@@ -18,26 +19,39 @@ COUNT_STRIDE = 4      # traverse.cuh kCountStride
 SPARSE_MAX = 24       # capi.cu far_sparse_max() default
 
 
-def _spread21(v):
-    v = v.astype(np.uint64) & np.uint64(0x1FFFFF)
-    for shift, mask in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
-                        (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
-        v = (v | (v << np.uint64(shift))) & np.uint64(mask)
-    return v
+KEY_LEVELS = 10      # tree.cu kKeyLevels
 
 
-def morton_batch_order(xyz):
-    """batch position -> original target index."""
+def key_batch_order(xyz):
+    """batch position -> original target index: the stable order of the 30-bit octree keys
+    (tree.cu k_geokey: ten bisections of the root cube of the points' tight box, k_root;
+    cluster_tree.hpp:99-105, 163-169, in the same rounded arithmetic)."""
     xyz = np.asarray(xyz, np.float64)
     lo, hi = xyz.min(axis=0), xyz.max(axis=0)
     side = 0.0
     for a in range(3):
-        side = max(side, hi[a] - lo[a])
-    inv = 2097151.0 / side if side > 0.0 else 0.0
-    key = np.zeros(len(xyz), np.uint64)
+        ext = hi[a] - lo[a]
+        side = ext if side < ext else side
+    side = side * (1.0 + 1e-12)
+    half = side * 0.5
+    blo = np.empty(3)
+    bhi = np.empty(3)
     for a in range(3):
-        q = np.minimum(np.maximum((xyz[:, a] - lo[a]) * inv, 0.0), 2097151.0).astype(np.uint64)
-        key |= _spread21(q) << np.uint64(2 - a)
+        c = (lo[a] + hi[a]) * 0.5
+        blo[a], bhi[a] = c - half, c + half
+    n = len(xyz)
+    key = np.zeros(n, np.uint64)
+    L = np.tile(blo, (n, 1))
+    H = np.tile(bhi, (n, 1))
+    for _ in range(KEY_LEVELS):
+        slot = np.zeros(n, np.uint64)
+        for a in range(3):
+            mid = (L[:, a] + H[:, a]) * 0.5
+            up = xyz[:, a] >= mid
+            slot |= up.astype(np.uint64) << np.uint64(a)
+            L[:, a] = np.where(up, mid, L[:, a])
+            H[:, a] = np.where(up, H[:, a], mid)
+        key = (key << np.uint64(3)) | slot
     return np.argsort(key, kind="stable").astype(np.int64)
 
 

@@ -684,9 +684,9 @@ def test_device_call_with_weights_in_flight(S):
     ("sphere", 9000, 150, 3, 0.7, 2, False),
 ])
 def test_shard_plan_matches_host_model(S, O, kind, n, n0, order, theta, world, disjoint):
-    """The batch order (Morton) and the work-balanced shard ranges the library computes on the
+    """The batch order (octree keys) and the work-balanced shard ranges the library computes on the
     GPU equal tests/shard_model.py's host restatement (which tests/test_multirank.py uses for
-    its gloo ranks): Morton keys, k_count's float32 cost model, st_shard_cuts."""
+    its gloo ranks): octree keys, k_count's integer cost model, st_shard_cuts."""
     import torch
     import shard_model as M
     ps = S.generate(kind, n, 21, True)
@@ -709,7 +709,7 @@ def test_shard_plan_matches_host_model(S, O, kind, n, n0, order, theta, world, d
         ranges.append((t0, t1))
     torch.cuda.synchronize()
     xyz = ps.position if tg is None else tg
-    order_ = M.morton_batch_order(xyz)
+    order_ = M.key_batch_order(xyz)
     assert np.array_equal(torig.cpu().numpy().astype(np.int64), order_)
     d = as_dict(ps)
     T = O.or_build_tree(d, n0, True)

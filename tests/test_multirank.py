@@ -1,10 +1,10 @@
 """CPU, world_size 2 over gloo: the N > 1 plumbing of bench.py / DESIGN.md "Multi-GPU".
 
-Every rank derives the same work-balanced cut of the Morton-ordered 32-target
+Every rank derives the same work-balanced cut of the key-ordered 32-target
 batches (no communication), owns a disjoint shard, and the batch-order slices
 are all-gathered (bench.allgather_batch_slices) and scattered to original order, so
 the combined result is bit-identical to the single-rank result.  The batch order and the
-cut use the CUDA path's own recipe (tests/shard_model.py: Morton keys, k_count's cost
+cut use the CUDA path's own recipe (tests/shard_model.py: octree keys, k_count's cost
 model, st_shard_cuts), pinned to the library by a GPU test; the per-target velocities
 here come from the oracle (no GPU in this container)."""
 import os
@@ -44,10 +44,10 @@ def _worker(rank, world, port, q):
     src = torch.from_numpy(ps.position.copy()) if rank == 0 else torch.zeros((n, 3), dtype=torch.float64)
     dist.broadcast(src, 0)
     assert np.array_equal(src.numpy(), ps.position)
-    # the CUDA path's batch order (Morton keys in the targets' tight box) and its per-warp
+    # the CUDA path's batch order (octree keys in the root cube of the targets' tight box) and its per-warp
     # cost model (k_count over the exact interaction lists), restated on the host and checked
     # against the library by tests/test_gpu_parity.py::test_shard_plan_matches_host_model
-    order = M.morton_batch_order(ps.position)
+    order = M.key_batch_order(ps.position)
     T = O.or_build_tree(d, n0, True)
     to_tree = np.empty(n, np.uint32)
     to_tree[T.to_original] = np.arange(n, dtype=np.uint32)
