@@ -95,6 +95,16 @@ def far_executed_flops(P):
     return 2 * fma + mul + add
 
 
+def far_lds_per_pair(P):
+    """Broadcast LDS.128 loads of folded weights per accepted pair in k_far_list<P>: two per
+    harmonic coefficient (four weight columns), one at the top grade (Psi only), two at grade
+    0 (csrc/far_eval.cuh).  221 at P = 10, matching the SASS."""
+    return 2 + sum(2 * (2 * n + 1) for n in range(1, P)) + (2 * P + 1)
+
+
+LDS128_CLK = 2.0  # SM clocks per warp-wide broadcast LDS.128 (scripts/micro/lds_split.cu, profiles/r02_lds_split.md)
+
+
 def moment_flops_per_incidence(p):
     """Reference-algorithmic flops per particle-cluster incidence of compute_moments
     (25 E(p) + 11, moments.hpp:34-80)."""
@@ -674,6 +684,20 @@ def run_gpu(args, cfg):
                                 "the same pairs; not a roofline fraction"}},
             "moments": moments,
             "near_s": near_s, "far_s": far_s}
+    # the far field's other ceiling: every weight reaches the lanes as a broadcast LDS.128,
+    # 2 SM clocks per warp instruction whatever the lanes' addresses -- above the DP pipe's
+    # 0.5 clock per DFMA at this instruction mix, so the shared-memory pipe binds first
+    sm_clk_hz = 1e6 * (clocks.summary().get("sm_mhz") or 0.0)
+    if far_s > 0 and sm_clk_hz > 0:
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        lds = far_lds_per_pair(P)
+        ceiling = sms * sm_clk_hz * 32.0 / (LDS128_CLK * lds)
+        achieved = stats.farfield_evals / far_s
+        roof["far"]["lds_bound"] = {
+            "lds128_per_pair": lds, "clk_per_warp_lds128": LDS128_CLK, "sms": sms, "sm_hz": sm_clk_hz,
+            "ceiling_pairs_per_s": ceiling, "achieved_pairs_per_s": achieved, "frac": achieved / ceiling,
+            "note": "pairs of both far kernels (k_feval's sparse events read weights from global memory) "
+                    "against the dense kernel's shared-memory ceiling at full lanes"}
     mine = {"rank": rank, "ms_per_step": my_ms / args.steps, "near_s": near_s, "far_s": far_s,
             "near_frac": roof["frac"], "far_frac": roof["far"]["frac"],
             "direct_pairs": stats.direct_pairs, "farfield_evals": stats.farfield_evals}
