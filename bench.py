@@ -569,11 +569,13 @@ def run_gpu(args, cfg):
             # positions (and targets) on the compute stream; the weight arrays on a side
             # stream, overlapping the tree build (st_treecode_velocity_device_ev waits for
             # them after the build, the way st_treecode_velocity_ex does for host arrays)
-            w_start.record(stream)
-            side.wait_event(w_start)  # the previous step is done with dsrc
             dsrc[:n].copy_(hsrc[:n], non_blocking=True)
             if dtg is not None:
                 dtg.copy_(htg, non_blocking=True)
+            # the weights start once the positions are in (the previous step is done with
+            # dsrc too): sharing the PCIe link with the positions would only delay the build
+            w_start.record(stream)
+            side.wait_event(w_start)
             with torch.cuda.stream(side):
                 dsrc[n:].copy_(hsrc[n:], non_blocking=True)
                 w_ready.record(side)

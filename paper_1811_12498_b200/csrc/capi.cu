@@ -1005,6 +1005,10 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
             dt.alloc(3 * nt, s);
             h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
         }
+        // ... after the positions: sharing the PCIe link with them would only delay the build
+        Event hpos;
+        hpos.record(s);
+        ST_CUDA(cudaStreamWaitEvent(s2, hpos.e, 0));
         d.f = sto ? up(src->force_weight, d.own_f, s2) : nullptr;
         d.h = str ? up(src->dipole_weight, d.own_h, s2) : nullptr;
         d.nu = str ? up(src->normal, d.own_nu, s2) : nullptr;
