@@ -22,7 +22,47 @@
 
 namespace st {
 thread_local uint64_t g_launches = 0;
+
+// pinned staging blocks of this host thread: `cur` is bumped; blocks outgrown during a
+// call are kept until the next reset (copies may still read them)
+struct PinnedArena {
+    struct Block {
+        char* p = nullptr;
+        size_t size = 0;
+    };
+    Block cur;
+    size_t used = 0;
+    std::vector<Block> old;
+    ~PinnedArena() {
+        for (auto& b : old) cudaFreeHost(b.p);
+        if (cur.p) cudaFreeHost(cur.p);
+    }
+};
+static thread_local PinnedArena g_pinned;
+
+void* pinned_stage(size_t bytes) {
+    PinnedArena& a = g_pinned;
+    bytes = (bytes + 15) & ~size_t(15);
+    if (a.used + bytes > a.cur.size) {
+        if (a.cur.p) a.old.push_back(a.cur);
+        const size_t sz = std::max<size_t>({bytes, 2 * a.cur.size, size_t(1) << 20});
+        void* p = nullptr;
+        ST_CUDA(cudaMallocHost(&p, sz));
+        a.cur = {static_cast<char*>(p), sz};
+        a.used = 0;
+    }
+    void* r = a.cur.p + a.used;
+    a.used += bytes;
+    return r;
 }
+
+void pinned_reset() {
+    PinnedArena& a = g_pinned;
+    for (auto& b : a.old) cudaFreeHost(b.p);
+    a.old.clear();
+    a.used = 0;
+}
+}  // namespace st
 
 using namespace st;
 
@@ -38,6 +78,7 @@ st_status set_error(st_status s, const std::string& m) {
 template <class F>
 st_status guarded(F&& f) {
     try {
+        pinned_reset();
         f();
         g_last_error.clear();
         return ST_OK;
@@ -484,8 +525,8 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         a.sparse_max = far_sparse_max();
         launch_count(a, (uint32_t)((P + 1) * (P + 1) * 8), s);
         launch_shard_cuts(cost.get(), nwarps, stride, nshards, dcuts.get(), s);
-        int wr[2] = {0, 0};
-        ST_CUDA(cudaMemcpyAsync(wr, dcuts.get() + shard, sizeof wr, cudaMemcpyDeviceToHost, s));
+        int* wr = static_cast<int*>(pinned_stage(2 * sizeof(int)));
+        ST_CUDA(cudaMemcpyAsync(wr, dcuts.get() + shard, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         ST_CUDA(cudaStreamSynchronize(s));
         a.w0 = wr[0];
         a.w1 = wr[1];
@@ -526,15 +567,18 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
         }
         DevArray<int32_t> d_rows(rows.size(), aux.s);
         if (!rows.empty())
-            ST_CUDA(cudaMemcpyAsync(d_rows.get(), rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, aux.s));
+            ST_CUDA(cudaMemcpyAsync(d_rows.get(), pinned_copy(rows.data(), rows.size()), rows.size() * 4,
+                                    cudaMemcpyHostToDevice, aux.s));
         fold_weights_rows_device(M.get(), d_rows.get(), (int)rows.size(), prm.order, sto, str, aux.s, W.get());
         d_units.alloc(sp.units.size(), aux.s);
-        ST_CUDA(cudaMemcpyAsync(d_units.get(), sp.units.data(), sp.units.size() * 4, cudaMemcpyHostToDevice, aux.s));
+        ST_CUDA(cudaMemcpyAsync(d_units.get(), pinned_copy(sp.units.data(), sp.units.size()), sp.units.size() * 4,
+                                cudaMemcpyHostToDevice, aux.s));
         Mu.alloc(sp.units.size() * m_row, aux.s);
         gather_rows_device(M.get(), d_units.get() + u0, (int)(u1 - u0), m_row, Mu.get() + u0 * m_row, false, aux.s);
         d_top.alloc(sp.top_ids.size(), aux.s);
         if (!sp.top_ids.empty())
-            ST_CUDA(cudaMemcpyAsync(d_top.get(), sp.top_ids.data(), sp.top_ids.size() * 4, cudaMemcpyHostToDevice,
+            ST_CUDA(cudaMemcpyAsync(d_top.get(), pinned_copy(sp.top_ids.data(), sp.top_ids.size()),
+                                    sp.top_ids.size() * 4, cudaMemcpyHostToDevice,
                                     aux.s));
     }
     e2.record(aux.s);
@@ -589,11 +633,16 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ro.t_far = tm.far_s;
     ro.t_near = tm.near_s;
     static const bool timeline = getenv("ST_DEBUG_TIMELINE") != nullptr;
-    if (timeline)  // ms from the call's first event: when each phase started / ended
+    if (timeline) {  // ms from the call's first event: when each phase started / ended
+        std::string plan;
+        for (size_t k = 0; k < tm.plan_ms.size(); ++k)
+            plan += std::string(" | ") + tm.plan_ms[k].first + " " + std::to_string(tm.plan_ms[k].second).substr(0, 6) +
+                    " (host +" + std::to_string(tm.plan_host_ms[k]).substr(0, 5) + ")";
         fprintf(stderr, "[timeline] build end %.3f | moments %.3f - %.3f (aux stream) | targets ordered %.3f | "
-                "cuts %.3f | near %.3f - %.3f | far start %.3f | end %.3f\n", 1e3 * ro.t_build, 1e3 * secs(e0, em),
-                1e3 * secs(e0, e2), 1e3 * secs(e0, et), 1e3 * secs(e0, ec), 1e3 * tm.near_start_s,
+                "cuts %.3f%s | near %.3f - %.3f | far start %.3f | end %.3f\n", 1e3 * ro.t_build, 1e3 * secs(e0, em),
+                1e3 * secs(e0, e2), 1e3 * secs(e0, et), 1e3 * secs(e0, ec), plan.c_str(), 1e3 * tm.near_start_s,
                 1e3 * (tm.near_start_s + tm.near_s), 1e3 * tm.far_start_s, 1e3 * ro.t_total);
+    }
     if (so) {
         so->w0 = a.w0;
         so->w1 = a.w1;

@@ -492,11 +492,13 @@ MomentsPlan plan_moments(const DevTree& tree, cudaStream_t s) {
     MomentsPlan pl;
     const int ncl = tree.ncl;
     // leaves: direct sums over their particles; internal clusters: M2M by level
-    std::vector<int4> info(ncl);
-    ST_CUDA(cudaMemcpyAsync(info.data(), tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> bylevel(ncl);
-    ST_CUDA(cudaMemcpyAsync(bylevel.data(), tree.bylevel.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
+    int4* hinfo = static_cast<int4*>(pinned_stage(sizeof(int4) * ncl));  // pinned: no staging stall
+    int32_t* hlvl = static_cast<int32_t*>(pinned_stage(sizeof(int32_t) * ncl));
+    ST_CUDA(cudaMemcpyAsync(hinfo, tree.info.get(), sizeof(int4) * ncl, cudaMemcpyDeviceToHost, s));
+    ST_CUDA(cudaMemcpyAsync(hlvl, tree.bylevel.get(), sizeof(int32_t) * ncl, cudaMemcpyDeviceToHost, s));
     ST_CUDA(cudaStreamSynchronize(s));
+    const std::vector<int4> info(hinfo, hinfo + ncl);
+    const std::vector<int32_t> bylevel(hlvl, hlvl + ncl);
     pl.depth.assign(ncl, 0);
     for (size_t d = 0; d + 1 < tree.level_start.size(); ++d)
         for (int b = tree.level_start[d]; b < tree.level_start[d + 1]; ++b) pl.depth[bylevel[b]] = (int)d;
@@ -621,14 +623,19 @@ void compute_moments_device(const DevTree& tree, const double* src, int p, bool 
     const std::vector<std::vector<int32_t>>& lv = plan->lv;
     const int nleaf = (int)cl.size();
     DevArray<int32_t> d_off(nleaf + 1, s), d_cl(nleaf, s), d_slot(nleaf, s), d_lvl(ncl, s);
-    ST_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), sizeof(int32_t) * (nleaf + 1), cudaMemcpyHostToDevice, s));
-    ST_CUDA(cudaMemcpyAsync(d_cl.get(), cl.data(), sizeof(int32_t) * nleaf, cudaMemcpyHostToDevice, s));
-    ST_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(int32_t) * nleaf, cudaMemcpyHostToDevice, s));
+    // pinned staging: a pageable upload would first wait for this stream to drain
+    ST_CUDA(cudaMemcpyAsync(d_off.get(), pinned_copy(off.data(), nleaf + 1), sizeof(int32_t) * (nleaf + 1),
+                            cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_cl.get(), pinned_copy(cl.data(), nleaf), sizeof(int32_t) * nleaf,
+                            cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemcpyAsync(d_slot.get(), pinned_copy(slot.data(), nleaf), sizeof(int32_t) * nleaf,
+                            cudaMemcpyHostToDevice, s));
     {
         std::vector<int32_t> flat;
         for (const auto& ids : lv) flat.insert(flat.end(), ids.begin(), ids.end());
         if (!flat.empty())
-            ST_CUDA(cudaMemcpyAsync(d_lvl.get(), flat.data(), sizeof(int32_t) * flat.size(), cudaMemcpyHostToDevice, s));
+            ST_CUDA(cudaMemcpyAsync(d_lvl.get(), pinned_copy(flat.data(), flat.size()), sizeof(int32_t) * flat.size(),
+                                    cudaMemcpyHostToDevice, s));
     }
     stamp("host lists");
     if (!keep) {

@@ -5,6 +5,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include <cstddef>
@@ -39,6 +40,22 @@ void shard_cuts_host(size_t n, const double* w, int k, size_t* cuts);
 // Kernel-launch counter (reported as st_stats.gpu_launches).
 extern thread_local uint64_t g_launches;
 inline void count_launch(uint64_t k = 1) { g_launches += k; }
+
+// Pinned host staging for the small host<->device transfers inside a call (plan lists up,
+// counts and cuts down).  A pageable transfer is not asynchronous: an upload first waits for
+// its stream to drain and a download goes through the driver's staging copy, so the host
+// stalls behind the other stream's kernels (measured: 2-2.4 ms at cfg2 / cfg4 before the
+// plan could be sized).  Per host thread, grow-only; pinned_reset() at each C-ABI entry
+// (every call synchronises its streams before returning, so the previous call's copies
+// are done with it).
+void* pinned_stage(size_t bytes);  // 16-byte aligned, valid until the next pinned_reset()
+void pinned_reset();
+template <class T>
+T* pinned_copy(const T* src, size_t n) {
+    T* p = static_cast<T*>(pinned_stage(n * sizeof(T)));
+    if (n) memcpy(p, src, n * sizeof(T));
+    return p;
+}
 
 // Timing event (move-only; destroyed with its owner).
 struct Event {

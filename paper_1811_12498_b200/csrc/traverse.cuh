@@ -3,6 +3,7 @@
 
 #include <functional>
 
+#include <utility>
 #include <vector>
 
 #include "st_common.cuh"
@@ -48,6 +49,10 @@ struct EvalTimes {
     std::vector<double> far_order;  // the same per order
     cudaEvent_t origin = nullptr;   // if set: start of the first near / far launch after it
     double near_start_s = 0.0, far_start_s = 0.0;
+    // ST_DEBUG_TIMELINE: ms from `origin` at the plan's steps (count walk done, plan sized
+    // on the host, write walk done)
+    std::vector<std::pair<const char*, double>> plan_ms;
+    std::vector<double> plan_host_ms;  // host clock at the same marks, from launch_eval's entry
 };
 // K3-K5 for the batch warps [a.w0, a.w1): the plan walks (counts, then near entries,
 // deferred sparse far entries and each warp's dense far events), then per slab the dense

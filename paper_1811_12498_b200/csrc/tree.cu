@@ -882,10 +882,12 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         DevArray<int32_t> actb[2] = {DevArray<int32_t>(mcap, s), DevArray<int32_t>(mcap, s)};
         DevArray<uint32_t> kseg((size_t)8 * mcap, s);
         DevArray<int32_t> kch(mcap + 1, s), kflag((size_t)8 * mcap + 1, s), kst(KS_LS + kKeyLevels + 2, s);
-        int32_t st0[KS_LS + kKeyLevels + 2] = {};
+        constexpr int NS = KS_LS + kKeyLevels + 2;
+        int32_t* st0 = static_cast<int32_t*>(pinned_stage(NS * sizeof(int32_t)));
+        memset(st0, 0, NS * sizeof(int32_t));
         st0[KS_M] = 1;
         st0[KS_TOTAL] = 1;
-        ST_CUDA(cudaMemcpyAsync(kst.get(), st0, sizeof st0, cudaMemcpyHostToDevice, s));
+        ST_CUDA(cudaMemcpyAsync(kst.get(), st0, NS * sizeof(int32_t), cudaMemcpyHostToDevice, s));
         ST_CUDA(cudaMemsetAsync(actb[0].get(), 0, sizeof(int32_t), s));
         KeyedLevels K;
         K.n0 = n0;
@@ -914,7 +916,9 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         ST_CUDA(cudaLaunchCooperativeKernel((const void*)k_keyed_levels, grid, kKeyThreads, args, 0, s));
         ST_LAUNCH("k_keyed_levels");
         count_launch();
-        ST_CUDA(cudaMemcpyAsync(st0, kst.get(), sizeof st0, cudaMemcpyDeviceToHost, s));
+        int32_t* st1 = static_cast<int32_t*>(pinned_stage(NS * sizeof(int32_t)));
+        ST_CUDA(cudaMemcpyAsync(st1, kst.get(), NS * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        st0 = st1;
         ST_CUDA(cudaStreamSynchronize(s));
         if (st0[KS_OVER]) fail(ST_RUNTIME_ERROR, "build_tree: keyed levels exceeded their bound");
         depth = st0[KS_DEPTH];
@@ -995,7 +999,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         ST_LAUNCH("k_children");
         launch_scan_i32(flag.get(), fpos.get(), Cmax, s);
         count_launch();
-        int32_t cm[2] = {0, 0};  // C, next level's split count
+        int32_t* cm = static_cast<int32_t*>(pinned_stage(2 * sizeof(int32_t)));  // C, next level's split count
         ST_CUDA(cudaMemcpyAsync(&cm[0], chbase.get() + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         ST_CUDA(cudaMemcpyAsync(&cm[1], fpos.get() + Cmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         ST_CUDA(cudaStreamSynchronize(s));
@@ -1150,8 +1154,8 @@ void order_targets(const double* d_pos, size_t n, cudaStream_t s, DevArray<uint3
     perm.alloc(n, s);
     if (!n) return;
     DevArray<unsigned long long> mm(6, s);
-    const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
-    ST_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof init, cudaMemcpyHostToDevice, s));
+    ST_CUDA(cudaMemsetAsync(mm.get(), 0xff, 3 * sizeof(unsigned long long), s));
+    ST_CUDA(cudaMemsetAsync(mm.get() + 3, 0x00, 3 * sizeof(unsigned long long), s));
     const unsigned g = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 8);
     k_tight_all<<<g, 256, 0, s>>>(d_pos, n, mm.get());
     ST_LAUNCH("k_tight_all");
