@@ -884,8 +884,33 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
             pool_grant_peer(da, db);
         }
     ST_CUDA(cudaSetDevice(dev0));
-    OwnedStream os0;
+    OwnedStream os0, os0w;
     cudaStream_t s0 = os0.s;
+    // the host arrays cross PCIe once, to device 0 (positions and targets first, the weight
+    // arrays after them on a second stream); every other device copies them from device 0
+    // over NVLink (peer copies) as each part lands
+    Event h0, pos_ready, w_ready0;
+    h0.record(s0);
+    DevParticles src0;
+    src0.n = src->n;
+    auto up0 = [&](const double* h, DevArray<double>& dst, cudaStream_t st) -> const double* {
+        if (!h) return nullptr;
+        dst.alloc(3 * src->n, st);
+        h2d(dst.get(), h, 3 * src->n * sizeof(double), st);
+        return dst.get();
+    };
+    src0.pos = up0(src->position, src0.own_pos, s0);
+    DevArray<double> tg0;
+    if (targets) {
+        tg0.alloc(3 * nt, s0);
+        h2d(tg0.get(), targets, 3 * nt * sizeof(double), s0);
+    }
+    pos_ready.record(s0);
+    ST_CUDA(cudaStreamWaitEvent(os0w.s, pos_ready.e, 0));
+    src0.f = sto ? up0(src->force_weight, src0.own_f, os0w.s) : nullptr;
+    src0.h = str ? up0(src->dipole_weight, src0.own_h, os0w.s) : nullptr;
+    src0.nu = str ? up0(src->normal, src0.own_nu, os0w.s) : nullptr;
+    w_ready0.record(os0w.s);
     DevArray<double> du(3 * nt, s0);
     DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s0);
     ST_CUDA(cudaStreamSynchronize(s0));  // allocations complete before other devices store into them
@@ -909,21 +934,44 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
             const int dev = (dev0 + d) % ndev;
             ST_CUDA(cudaSetDevice(dev));
             ensure_device();
-            OwnedStream os;
+            OwnedStream os, os2;
             cudaStream_t s = d == 0 ? s0 : os.s;
-            DevParticles dp;
-            upload(src, sto, str, dp, s);
-            DevArray<double> dt;
-            if (targets) {
-                dt.alloc(3 * nt, s);
-                h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
-            }
             pctx[d] = PeerCtx{&grp, d};
             SplitExchange x;
             x.fn = peer_exchange;
             x.ctx = &pctx[d];
-            run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d, D,
-                         s, ros[d], false, nullptr, nullptr, &x);
+            if (d == 0) {
+                run_treecode(src0, targets ? tg0.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr,
+                             d, D, s, ros[d], false, nullptr, w_ready0.e, &x);
+            } else {
+                // device 0's copies, peer to peer: positions (and targets) on the compute stream,
+                // the weight arrays on a second stream that run_treecode waits for after the build
+                DevParticles dp;
+                dp.n = src->n;
+                auto peer = [&](const double* from, DevArray<double>& dst, cudaStream_t st) -> const double* {
+                    if (!from) return nullptr;
+                    dst.alloc(3 * src->n, st);
+                    ST_CUDA(cudaMemcpyPeerAsync(dst.get(), dev, from, dev0, 3 * src->n * sizeof(double), st));
+                    return dst.get();
+                };
+                ST_CUDA(cudaStreamWaitEvent(s, pos_ready.e, 0));
+                dp.pos = peer(src0.pos, dp.own_pos, s);
+                DevArray<double> dt;
+                if (targets) {
+                    dt.alloc(3 * nt, s);
+                    ST_CUDA(cudaMemcpyPeerAsync(dt.get(), dev, tg0.get(), dev0, 3 * nt * sizeof(double), s));
+                }
+                ST_CUDA(cudaStreamWaitEvent(os2.s, w_ready0.e, 0));
+                dp.f = peer(src0.f, dp.own_f, os2.s);
+                dp.h = peer(src0.h, dp.own_h, os2.s);
+                dp.nu = peer(src0.nu, dp.own_nu, os2.s);
+                Event wd;
+                wd.record(os2.s);
+                run_treecode(dp, targets ? dt.get() : nullptr, nt, prm, du.get(), per_target ? dpt.get() : nullptr, d,
+                             D, s, ros[d], false, nullptr, wd.e, &x);
+                // the weight copies' stream-ordered frees are on os2: wait before it goes
+                ST_CUDA(cudaStreamSynchronize(os2.s));
+            }
             raise_flags(ros[d]);
         } catch (...) {
             errs[d] = std::current_exception();
@@ -948,7 +996,7 @@ void multi_device(const st_particles* src, const double* targets, size_t n_targe
     d1.record(s0);
     ST_CUDA(cudaStreamSynchronize(s0));
     t_d2h = secs(d0, d1);
-    t_h2d = 0.0;
+    t_h2d = secs(h0, w_ready0);  // the one PCIe upload (device 0); the rest moved over NVLink
     for (const RunOut& r : ros) {
         for (int k = 0; k < 3; ++k) ro_all.stats[k] += r.stats[k];
         ro_all.t_build = std::max(ro_all.t_build, r.t_build);
