@@ -96,13 +96,22 @@ def far_executed_flops(P):
 
 
 def far_lds_per_pair(P):
-    """Broadcast LDS.128 loads of folded weights per accepted pair in k_far_list<P>: two per
-    harmonic coefficient (four weight columns), one at the top grade (Psi only), two at grade
-    0 (csrc/far_eval.cuh).  221 at P = 10, matching the SASS."""
-    return 2 + sum(2 * (2 * n + 1) for n in range(1, P)) + (2 * P + 1)
+    """Broadcast shared-memory loads of folded weights per accepted pair in k_far_list<P>
+    (csrc/far_eval.cuh): (LDS.128, LDS.64).  Two LDS.128 per harmonic coefficient (four
+    weight columns); the top grade's lone Psi column and grade 0's third Phi column as
+    LDS.64.  (199, 22) at P = 10, matching the SASS."""
+    return 1 + sum(2 * (2 * n + 1) for n in range(1, P)), 1 + (2 * P + 1)
 
 
-LDS128_CLK = 2.0  # SM clocks per warp-wide broadcast LDS.128 (scripts/micro/lds_split.cu, profiles/r02_lds_split.md)
+def far_lds_clk_per_pair(P):
+    """SM clocks per warp event the weight loads hold the shared-memory pipe: a broadcast
+    LDS.128 costs 2, an LDS.64 1 (scripts/micro/lds_split.cu, profiles/r02_lds_split.md)."""
+    l128, l64 = far_lds_per_pair(P)
+    return LDS128_CLK * l128 + LDS64_CLK * l64
+
+
+LDS128_CLK = 2.0  # SM clocks per warp-wide broadcast LDS.128 (profiles/r02_lds_split.md)
+LDS64_CLK = 1.0   # ... per broadcast LDS.64
 
 
 def moment_flops_per_incidence(p):
@@ -686,17 +695,20 @@ def run_gpu(args, cfg):
                                 "the same pairs; not a roofline fraction"}},
             "moments": moments,
             "near_s": near_s, "far_s": far_s}
-    # the far field's other ceiling: every weight reaches the lanes as a broadcast LDS.128,
-    # 2 SM clocks per warp instruction whatever the lanes' addresses -- above the DP pipe's
-    # 0.5 clock per DFMA at this instruction mix, so the shared-memory pipe binds first
+    # the far field's other ceiling: every weight reaches the lanes as a broadcast
+    # shared-memory load, 2 SM clocks per warp-wide LDS.128 and 1 per LDS.64 whatever the
+    # lanes' addresses -- above the DP pipe's 0.5 clock per DFMA at this instruction mix, so
+    # the shared-memory pipe binds first
     sm_clk_hz = 1e6 * (clocks.summary().get("sm_mhz") or 0.0)
     if far_s > 0 and sm_clk_hz > 0:
         sms = torch.cuda.get_device_properties(local).multi_processor_count
-        lds = far_lds_per_pair(P)
-        ceiling = sms * sm_clk_hz * 32.0 / (LDS128_CLK * lds)
+        l128, l64 = far_lds_per_pair(P)
+        clk = far_lds_clk_per_pair(P)
+        ceiling = sms * sm_clk_hz * 32.0 / clk
         achieved = stats.farfield_evals / far_s
         roof["far"]["lds_bound"] = {
-            "lds128_per_pair": lds, "clk_per_warp_lds128": LDS128_CLK, "sms": sms, "sm_hz": sm_clk_hz,
+            "lds128_per_pair": l128, "lds64_per_pair": l64, "clk_per_warp_event": clk,
+            "clk_per_warp_lds128": LDS128_CLK, "clk_per_warp_lds64": LDS64_CLK, "sms": sms, "sm_hz": sm_clk_hz,
             "ceiling_pairs_per_s": ceiling, "achieved_pairs_per_s": achieved, "frac": achieved / ceiling,
             "note": "pairs of both far kernels (k_feval's sparse events read weights from global memory) "
                     "against the dense kernel's shared-memory ceiling at full lanes"}

@@ -82,3 +82,40 @@ def test_far_executed_flops_match_sass(kernel, P):
         # the packed sparse pass recomputes r^2 with its own DMULs: at most 3 flops more per
         # pair, so the dense kernel's count used for both slightly under-counts (<= 2%)
         assert bench.far_executed_flops(P) <= flops <= bench.far_executed_flops(P) + 3, (kernel, P, dict(ops))
+
+
+def innermost_pair_loop_mnemonics(lines):
+    """The same loop as innermost_pair_loop, counted by full mnemonic (LDS.128 vs LDS.64)."""
+    ins = []
+    for ln in lines:
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(2).strip()))
+    addr = {a: i for i, (a, _) in enumerate(ins)}
+    best = None
+    for i, (a, txt) in enumerate(ins):
+        m = re.search(r"BRA\s.*?0x([0-9a-f]+)", txt)
+        if not m:
+            continue
+        tgt = int(m.group(1), 16)
+        if tgt > a or tgt not in addr:
+            continue
+        body = ins[addr[tgt]:i + 1]
+        full = collections.Counter(t.split()[1 if t.startswith("@") else 0] for _, t in body)
+        if sum(v for k, v in full.items() if k.startswith("MUFU")) != 1:
+            continue
+        if best is None or len(body) < best[0]:
+            best = (len(body), full)
+    return best[1] if best else None
+
+
+@pytest.mark.parametrize("P", [3, 7, 9, 10, 12])
+def test_far_weight_loads_match_sass(P):
+    """bench.py's far-field shared-memory ceiling counts the broadcast weight loads per pair
+    (bench.far_lds_per_pair): pinned to k_far_list<P>'s event loop."""
+    import bench
+    name = next((f for f in funcs() if re.search(rf"k_far_listILi{P}E", f)), None)
+    assert name
+    ops = innermost_pair_loop_mnemonics(funcs()[name])
+    assert ops is not None
+    assert (ops.get("LDS.128", 0), ops.get("LDS.64", 0)) == bench.far_lds_per_pair(P), (P, dict(ops))
