@@ -18,7 +18,7 @@ accuracy : the other half of the BASELINE metric -- relative L2 error against th
 --gpus N (N > 1) without torchrun re-launches itself under torch.distributed.run with
 N ranks (NCCL; gloo when the box has fewer than N GPUs, ranks then share them).  Every
 rank rebuilds the tree and moments (bit-identical) and evaluates its work-balanced shard
-of the Morton-ordered target batches; the epilogue kernel stores each shard straight
+of the key-ordered target batches; the epilogue kernel stores each shard straight
 into rank 0's output over NVLink (CUDA IPC), or --gather nccl all-gathers batch-order
 slices.
 
@@ -382,7 +382,7 @@ def config_block(cfg, args, world):
     par = "one GPU"
     if world > 1:
         split = args.gather == "peer" and args.moments == "split"
-        par = (f"targets sharded over {world} GPUs by work-balanced Morton batches, tree replicated, "
+        par = (f"targets sharded over {world} GPUs by work-balanced key-ordered batches, tree replicated, "
                + ("moment pass split by subtrees with the weight rows exchanged over NCCL" if split
                   else "moments replicated")
                + (", shards stored into rank 0's output by the epilogue kernel (CUDA IPC, NVLink)"
@@ -509,7 +509,7 @@ def run_gpu(args, cfg):
                                                n_shards=world, stream=sptr)
             dist.all_reduce(done)  # every shard's stores into rank 0's buffer have completed
             return r
-        # every rank: same tree/moments, its work-balanced slice of the Morton-ordered batches in
+        # every rank: same tree/moments, its work-balanced slice of the key-ordered batches in
         # batch order; NCCL all-gather of the slices over NVLink; scatter to original order
         t0, t1, r = S.treecode_shard_device(*ptrs, n, prm, dbatch.data_ptr(), torig.data_ptr(), targets_ptr=tp,
                                             n_targets=ntp, shard=rank, n_shards=world, stream=sptr)

@@ -121,7 +121,7 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
 /* Device-resident form: every pointer (src arrays, targets, u_out) is device
  * memory on the current device; work is issued on `stream` (cudaStream_t,
  * NULL = the legacy default stream).  shard / n_shards select a contiguous,
- * work-balanced range of the Morton-ordered target batches (n_shards = 1:
+ * work-balanced range of the key-ordered target batches (n_shards = 1:
  * all); only that shard's entries of u_out are written.  This is the entry a
  * multi-process (one rank per GPU) driver uses; the tree and moments are
  * rebuilt redundantly and bit-identically on every rank. */
@@ -191,7 +191,7 @@ st_status st_treecode_velocity_device_split(const st_particles* src_device, cons
 
 /* Shard evaluation for collective gathers (one rank per GPU): like
  * st_treecode_velocity_device but the shard's velocities are written in BATCH order
- * (Morton order of 32-target batches) into u_batch[3*t0 .. 3*t1), so every rank owns a
+ * (octree-key order of 32-target batches) into u_batch[3*t0 .. 3*t1), so every rank owns a
  * contiguous slice [t0, t1) that an all-gather can move; batch_to_original (device,
  * n_targets uint32, optional) receives the permutation, identical on every rank. */
 st_status st_treecode_shard_device(const st_particles* src_device, const double* targets_device,
