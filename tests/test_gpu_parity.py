@@ -29,12 +29,66 @@ def tree_equal(T_gpu, T_ref):
     ("cube", 10000, 500, True), ("cube", 10000, 500, False), ("unit", 3000, 1, True),
     ("sphere", 20000, 200, True), ("sphere", 20000, 200, False), ("mixture", 50000, 100, True),
     ("cube", 200000, 2000, True), ("unit", 7, 1, True),
+    # > 64K splitting segments possible (n / (N0+1)): the keyed levels by the host loop, then
+    # the partition passes below depth 10
+    ("cube", 140000, 1, True),
 ])
 def test_tree_bit_exact(S, need_ref, kind, n, n0, shrink):
     ps = S.generate(kind, n, 12345, True)
     T = S.build_tree(ps, n0, shrink)
     ctx = need_ref.RefContext(as_dict(ps), 0, 0.5, n0, shrink)
     tree_equal(T, ctx.tree())
+
+
+def test_tree_coincident_points_reach_depth_64(S, need_ref):
+    """3,000 copies of one point among 2,000 others: the reference splits them until its
+    depth cap (leaf iff count <= N0 or depth >= 64, cluster_tree.hpp:96) -- 54 partition
+    levels below the keyed ones."""
+    rng = np.random.default_rng(5)
+    pos = np.concatenate([rng.uniform(-1, 1, (2000, 3)), np.tile([[0.125, -0.25, 0.375]], (3000, 1))])
+    pos = pos[rng.permutation(len(pos))]
+    nu = rng.normal(size=pos.shape)
+    nu /= np.linalg.norm(nu, axis=1, keepdims=True)
+    ps = S.ParticleSet(pos, rng.uniform(-1, 1, pos.shape), rng.uniform(-1, 1, pos.shape), nu)
+    T = S.build_tree(ps, 50, True)
+    ctx = need_ref.RefContext(as_dict(ps), 0, 0.5, 50, True)
+    R = ctx.tree()
+    tree_equal(T, R)
+    assert T.is_leaf.sum() > 0 and T.ncl > 64
+
+
+_BUILD_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1811_12498_b200 as S
+kind, n, n0 = sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
+T = S.build_tree(S.generate(kind, n, 12345, True), n0, True)
+np.savez(sys.argv[5], to_original=T.to_original, begin=T.begin, end=T.end, children=T.children,
+         geom=T.geom)
+"""
+
+
+@pytest.mark.parametrize("env", ["ST_TREE_PARTITION", "ST_TREE_LEVEL_LOOP"])
+@pytest.mark.parametrize("kind,n,n0", [("cube", 50000, 100), ("mixture", 30000, 20), ("unit", 3000, 1)])
+def test_tree_build_variants_bit_exact(S, need_ref, tmp_path, env, kind, n, n0):
+    """The A/B switches of the build (partition passes from the root; the keyed levels by the
+    host loop instead of the cooperative launch) give the same trees (env read once per
+    process: a subprocess per variant)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "t.npz"
+    r = subprocess.run([sys.executable, "-c", _BUILD_SNIPPET, root, kind, str(n), str(n0), str(out)],
+                       env=dict(os.environ, **{env: "1"}), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    ps = S.generate(kind, n, 12345, True)
+    R = need_ref.RefContext(as_dict(ps), 0, 0.5, n0, True).tree()
+    assert np.array_equal(got["to_original"], R.to_original)
+    assert np.array_equal(got["begin"], R.begin) and np.array_equal(got["end"], R.end)
+    assert np.array_equal(got["children"], R.children)
+    assert np.array_equal(got["geom"].view(np.uint64), R.geom.view(np.uint64))
 
 
 def test_tree_corner_cases(S, need_ref):
