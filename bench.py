@@ -571,6 +571,7 @@ def run_gpu(args, cfg):
 
     side = torch.cuda.Stream() if world == 1 else None
     w_ready = torch.cuda.Event() if world == 1 else None
+    t_ready = torch.cuda.Event() if world == 1 else None
     w_start = torch.cuda.Event() if world == 1 else None
 
     def e2e_step():
@@ -579,19 +580,22 @@ def run_gpu(args, cfg):
             # stream, overlapping the tree build (st_treecode_velocity_device_ev waits for
             # them after the build, the way st_treecode_velocity_ex does for host arrays)
             dsrc[:n].copy_(hsrc[:n], non_blocking=True)
-            if dtg is not None:
-                dtg.copy_(htg, non_blocking=True)
-            # the weights start once the positions are in (the previous step is done with
-            # dsrc too): sharing the PCIe link with the positions would only delay the build
+            # disjoint targets, then the weights, start once the positions are in (the
+            # previous step is done with dsrc and dtg too): sharing the PCIe link with the
+            # positions would only delay the build; the targets' ordering runs beside it
             w_start.record(stream)
             side.wait_event(w_start)
             with torch.cuda.stream(side):
+                if dtg is not None:
+                    dtg.copy_(htg, non_blocking=True)
+                    t_ready.record(side)
                 dsrc[n:].copy_(hsrc[n:], non_blocking=True)
                 w_ready.record(side)
             tp = None if dtg is None else dtg.data_ptr()
             S.treecode_velocity_device(*ptrs, n, prm, dout.data_ptr(), targets_ptr=tp,
                                        n_targets=nt if dtg is not None else 0, stream=sptr,
-                                       weights_event=w_ready.cuda_event)
+                                       weights_event=w_ready.cuda_event,
+                                       targets_event=t_ready.cuda_event if dtg is not None else 0)
             hout.copy_(dout, non_blocking=True)
             return
         if rank == 0:
@@ -626,8 +630,9 @@ def run_gpu(args, cfg):
         assert np.isfinite(u_e2e).all()
     e2e = {"value": e2e_val, "unit": "targets/s", "h2d_bytes_per_step": int(h2d_bytes) if rank == 0 else 0,
            "d2h_bytes_per_step": int(d2h_bytes),
-           "path": "st_treecode_velocity_device_ev with per-step H2D of pinned particle arrays (positions "
-                   "first, weights on a side stream overlapping the tree build) and D2H of the velocities "
+           "path": "st_treecode_velocity_device_ev2 with per-step H2D of pinned particle arrays (positions "
+                   "first; disjoint targets, then the weights, on a side stream overlapping the tree build) and "
+                   "D2H of the velocities "
                    "(CUDA events, max over ranks)",
            "step_ms": [round(a.elapsed_time(b), 3) for a, b in ee]}
     if world == 1:

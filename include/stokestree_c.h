@@ -138,6 +138,14 @@ st_status st_treecode_velocity_device_ev(const st_particles* src_device, const d
                                          size_t n_targets, const st_params* params,
                                          double* u_out_device, int shard, int n_shards,
                                          void* stream, void* weights_ready, st_stats* stats);
+/* As st_treecode_velocity_device_ev while the disjoint targets may also still be in flight:
+ * the call waits for `targets_ready` (a cudaEvent_t, may be NULL) before it orders them --
+ * beside the tree build, which then needs only the positions to have landed. */
+st_status st_treecode_velocity_device_ev2(const st_particles* src_device, const double* targets_device,
+                                          size_t n_targets, const st_params* params,
+                                          double* u_out_device, int shard, int n_shards,
+                                          void* stream, void* targets_ready, void* weights_ready,
+                                          st_stats* stats);
 
 /* Order sweep (new): velocities at every order in orders[n_orders] (params->order
  * ignored) from one tree, one moment pass at max(orders) -- order-p moments are the

@@ -59,7 +59,7 @@ lib_path = os.environ.get("ST_LIB_PATH") or os.path.join(_HERE, "libstokestree_b
 EXPORTED_SYMBOLS = (
     "st_abi_version", "st_last_error", "st_device_count", "st_params_validate",
     "st_treecode_velocity", "st_treecode_velocity_ex", "st_treecode_velocity_device",
-    "st_treecode_velocity_device_ev",
+    "st_treecode_velocity_device_ev", "st_treecode_velocity_device_ev2",
     "st_direct_velocity", "st_direct_velocity_at", "st_naive_direct_velocity", "st_build_tree",
     "st_tree_num_clusters", "st_tree_num_particles", "st_tree_export", "st_tree_free",
     "st_compute_moments", "st_coulomb_coeffs", "st_farfield_pairs", "st_relative_error",
@@ -144,6 +144,8 @@ def load_library():
     L.st_treecode_velocity_ex.argtypes = [P(_Particles), vp, sz, P(_Params), vp, vp, P(_Stats)]
     L.st_treecode_velocity_device.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, i, vp, P(_Stats)]
     L.st_treecode_velocity_device_ev.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, i, vp, vp, P(_Stats)]
+    L.st_treecode_velocity_device_ev2.argtypes = [P(_Particles), vp, sz, P(_Params), vp, i, i, vp, vp, vp,
+                                                  P(_Stats)]
     L.st_direct_velocity.argtypes = [P(_Particles), i, i, sz, sz, vp]
     L.st_direct_velocity_at.argtypes = [P(_Particles), i, i, vp, sz, vp]
     L.st_naive_direct_velocity.argtypes = [P(_Particles), i, i, vp]
@@ -416,16 +418,20 @@ def ipc_close(device_ptr: int) -> None:
 def treecode_velocity_device(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],
                              normal_ptr: Optional[int], n: int, params: TreecodeParams, u_out_ptr: int,
                              targets_ptr: Optional[int] = None, n_targets: int = 0, shard: int = 0,
-                             n_shards: int = 1, stream: int = 0, weights_event: int = 0) -> VelocityResult:
+                             n_shards: int = 1, stream: int = 0, weights_event: int = 0,
+                             targets_event: int = 0) -> VelocityResult:
     """Device-resident call: raw device pointers (e.g. torch ``data_ptr()``) and a CUDA stream.
     weights_event (a cudaEvent_t handle, e.g. torch.cuda.Event.cuda_event): the weight
-    arrays may still be in flight until it completes (st_treecode_velocity_device_ev)."""
+    arrays may still be in flight until it completes (st_treecode_velocity_device_ev);
+    targets_event: likewise the disjoint targets, waited for before they are ordered
+    (st_treecode_velocity_device_ev2)."""
     L = load_library()
     cp = _Particles(n, position_ptr, force_ptr, dipole_ptr, normal_ptr)
     prm = params._c()
     st = _Stats()
-    _check(L.st_treecode_velocity_device_ev(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr,
-                                            shard, n_shards, stream, weights_event or None, C.byref(st)))
+    _check(L.st_treecode_velocity_device_ev2(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr,
+                                             shard, n_shards, stream, targets_event or None, weights_event or None,
+                                             C.byref(st)))
     return _result(None, st)
 
 

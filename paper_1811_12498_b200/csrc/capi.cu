@@ -426,7 +426,8 @@ struct SplitExchange {
 void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in, const st_params& prm,
                   double* d_out, uint64_t* d_per_target, int shard, int nshards, cudaStream_t s,
                   RunOut& ro, bool out_batch = false, ShardOut* so = nullptr,
-                  cudaEvent_t weights_ready = nullptr, const SplitExchange* xchg = nullptr) {
+                  cudaEvent_t weights_ready = nullptr, const SplitExchange* xchg = nullptr,
+                  cudaEvent_t targets_ready = nullptr) {
     const bool sto = prm.stokeslet != 0, str = prm.stresslet != 0;
     const size_t n = src.n;
     const bool same = d_targets == nullptr;
@@ -441,7 +442,10 @@ void run_treecode(const DevParticles& src, const double* d_targets, size_t nt_in
     ST_CUDA(cudaStreamWaitEvent(aux.s, e0.e, 0));
     const double* tpos = same ? src.pos : d_targets;
     DevArray<uint32_t> tperm;
-    if (!same) order_targets(tpos, nt, aux.s, tperm);
+    if (!same) {
+        if (targets_ready) ST_CUDA(cudaStreamWaitEvent(aux.s, targets_ready, 0));
+        order_targets(tpos, nt, aux.s, tperm);
+    }
     Event esort;
     esort.record(aux.s);
 
@@ -1097,15 +1101,17 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
         };
         d.pos = up(src->position, d.own_pos, s);
         const size_t nt = targets ? n_targets : src->n;
-        DevArray<double> dt;
-        if (targets) {
-            dt.alloc(3 * nt, s);
-            h2d(dt.get(), targets, 3 * nt * sizeof(double), s);
-        }
-        // ... after the positions: sharing the PCIe link with them would only delay the build
-        Event hpos;
+        // ... after the positions: sharing the PCIe link with them would only delay the build.
+        // Disjoint targets next (their ordering runs beside the build), then the weights.
+        Event hpos, tready;
         hpos.record(s);
         ST_CUDA(cudaStreamWaitEvent(s2, hpos.e, 0));
+        DevArray<double> dt;
+        if (targets) {
+            dt.alloc(3 * nt, s2);
+            h2d(dt.get(), targets, 3 * nt * sizeof(double), s2);
+            tready.record(s2);
+        }
         d.f = sto ? up(src->force_weight, d.own_f, s2) : nullptr;
         d.h = str ? up(src->dipole_weight, d.own_h, s2) : nullptr;
         d.nu = str ? up(src->normal, d.own_nu, s2) : nullptr;
@@ -1114,7 +1120,7 @@ st_status st_treecode_velocity_ex(const st_particles* src, const double* targets
         DevArray<uint64_t> dpt(per_target ? 3 * nt : 0, s);
         RunOut ro;
         run_treecode(d, targets ? dt.get() : nullptr, nt, *params, du.get(), per_target ? dpt.get() : nullptr, 0,
-                     1, s, ro, false, nullptr, wready.e);
+                     1, s, ro, false, nullptr, wready.e, nullptr, targets ? tready.e : nullptr);
         raise_flags(ro);
         d0.record(s);
         d2h(u_out, du.get(), 3 * nt * sizeof(double), s);
@@ -1287,6 +1293,14 @@ st_status st_treecode_velocity_device(const st_particles* src, const double* tar
 st_status st_treecode_velocity_device_ev(const st_particles* src, const double* targets, size_t n_targets,
                                          const st_params* params, double* u_out, int shard, int n_shards,
                                          void* stream, void* weights_ready, st_stats* stats) {
+    return st_treecode_velocity_device_ev2(src, targets, n_targets, params, u_out, shard, n_shards, stream, nullptr,
+                                           weights_ready, stats);
+}
+
+st_status st_treecode_velocity_device_ev2(const st_particles* src, const double* targets, size_t n_targets,
+                                          const st_params* params, double* u_out, int shard, int n_shards,
+                                          void* stream, void* targets_ready, void* weights_ready,
+                                          st_stats* stats) {
     return guarded([&] {
         g_launches = 0;
         validate_params(params);
@@ -1304,7 +1318,8 @@ st_status st_treecode_velocity_device_ev(const st_particles* src, const double* 
         d.nu = str ? src->normal : nullptr;
         RunOut ro;
         run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro,
-                     false, nullptr, static_cast<cudaEvent_t>(weights_ready));
+                     false, nullptr, static_cast<cudaEvent_t>(weights_ready), nullptr,
+                     static_cast<cudaEvent_t>(targets_ready));
         raise_flags(ro);
         fill_stats(stats, ro);
         if (stats) stats->gpu_launches = g_launches;
