@@ -592,6 +592,10 @@ __global__ void __launch_bounds__(kKeyThreads) k_keyed_levels(const KeyedLevels 
                 for (int k = 0; k < 8; ++k) {
                     const uint32_t st = K.seg_cnt[8 * sg + k], en = k == 7 ? e : K.seg_cnt[8 * sg + k + 1];
                     c += en > st;
+#ifdef ST_DEBUG_CHECKS
+                    // slot ranges tile the parent's range in slot order (debug builds)
+                    if (en < st || (k == 0 && st != K.nb_begin[act[sg]])) K.state[KS_OVER] = 2;
+#endif
                 }
                 K.chbase[sg] = c;
             }
@@ -920,6 +924,7 @@ void build_tree_device(const double* d_pos, size_t n_sz, int n0, bool shrink, bo
         ST_CUDA(cudaMemcpyAsync(st1, kst.get(), NS * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         st0 = st1;
         ST_CUDA(cudaStreamSynchronize(s));
+        if (st0[KS_OVER] == 2) fail(ST_RUNTIME_ERROR, "build_tree: keyed levels' slot ranges do not tile a segment");
         if (st0[KS_OVER]) fail(ST_RUNTIME_ERROR, "build_tree: keyed levels exceeded their bound");
         depth = st0[KS_DEPTH];
         for (int d = 1; d <= depth; ++d) level_start.push_back(st0[KS_LS + d]);
