@@ -222,6 +222,27 @@ st_status st_ipc_export(const void* device_ptr, unsigned char handle[64], size_t
 st_status st_ipc_open(const unsigned char handle[64], size_t offset, void** device_ptr);
 st_status st_ipc_close(void* device_ptr);
 
+/* ---- one process per GPU with NCCL inside the library (no torch.distributed needed) ----
+ * Rank 0 calls st_nccl_unique_id and ships the 128-byte id to the other ranks by any means
+ * (a file, a socket, MPI); every rank then calls st_nccl_comm_init(id, n_ranks, rank) with
+ * its GPU current.  The library loads libnccl.so.2 at first use (the copy already in the
+ * process when PyTorch is, else the system's); failures return ST_NCCL_ERROR. */
+typedef struct st_comm st_comm;
+st_status st_nccl_unique_id(unsigned char id[128]);
+st_status st_nccl_comm_init(const unsigned char id[128], int n_ranks, int rank, st_comm** comm);
+void st_nccl_comm_free(st_comm* comm);
+/* The treecode on one rank of `comm` (replaces engine.hpp:157-169's worker threads over one
+ * output with one rank per GPU): every rank holds all sources (and targets) on its device;
+ * the moment pass is split over the ranks, its weight rows and subtree-root moments moved
+ * by NCCL broadcasts on `stream`; the rank evaluates its work-balanced shard of the
+ * key-ordered target batches; u_out (device, on every rank) receives every target's
+ * velocity in original order and stats the whole job's counters (one NCCL sum: each
+ * target has exactly one writer, so the values are one GPU's -- except that a component
+ * exactly -0.0 comes back +0.0).  Every rank must make the call (collective). */
+st_status st_treecode_velocity_nccl(const st_particles* src_device, const double* targets_device,
+                                    size_t n_targets, const st_params* params, double* u_out_device,
+                                    const st_comm* comm, void* stream, st_stats* stats);
+
 /* ---- direct sums (O(N^2) oracle path) ---- */
 /* contracted_direct_velocity(ps, sel, first, last) (kernels.hpp:123-136). */
 st_status st_direct_velocity(const st_particles* src, int stokeslet, int stresslet, size_t first,

@@ -67,7 +67,8 @@ EXPORTED_SYMBOLS = (
     "st_sphere_count", "st_generate_sphere_icosa", "st_generate_cube_density", "st_write_particles",
     "st_read_particles", "st_loaded_copy", "st_loaded_free", "st_treecode_shard_device", "st_unbatch_device",
     "st_taylor_coeffs", "st_ipc_export", "st_ipc_open", "st_ipc_close", "st_release_workspace",
-    "st_treecode_velocity_device_split",
+    "st_treecode_velocity_device_split", "st_nccl_unique_id", "st_nccl_comm_init", "st_nccl_comm_free",
+    "st_treecode_velocity_nccl",
 )
 
 GEN_UNIT, GEN_CUBE, GEN_SPHERE, GEN_MIXTURE, GEN_POINTS = range(5)
@@ -173,6 +174,11 @@ def load_library():
     L.st_ipc_export.argtypes = [vp, C.c_char_p, C.POINTER(sz)]
     L.st_ipc_open.argtypes = [C.c_char_p, sz, C.POINTER(vp)]
     L.st_ipc_close.argtypes = [vp]
+    L.st_nccl_unique_id.argtypes = [C.c_char_p]
+    L.st_nccl_comm_init.argtypes = [C.c_char_p, i, i, P(vp)]
+    L.st_nccl_comm_free.argtypes = [vp]
+    L.st_nccl_comm_free.restype = None
+    L.st_treecode_velocity_nccl.argtypes = [P(_Particles), vp, sz, P(_Params), vp, vp, vp, P(_Stats)]
     L.st_sphere_count.restype = sz
     L.st_sphere_count.argtypes = [i]
     L.st_generate_sphere_icosa.argtypes = [i, C.c_uint64, vp, vp, vp, vp]
@@ -390,6 +396,51 @@ def treecode_shard_device(position_ptr, force_ptr, dipole_ptr, normal_ptr, n, pa
 
 def unbatch_device(n, batch_to_original_ptr, u_batch_ptr, u_out_ptr, stream=0):
     _check(load_library().st_unbatch_device(n, batch_to_original_ptr, u_batch_ptr, u_out_ptr, stream))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id (st_nccl_unique_id): rank 0 makes it, every rank passes it to NcclComm."""
+    b = C.create_string_buffer(128)
+    _check(load_library().st_nccl_unique_id(b))
+    return b.raw
+
+
+class NcclComm:
+    """The library's own NCCL communicator (st_nccl_comm_init) on the current CUDA device."""
+
+    def __init__(self, unique_id: bytes, n_ranks: int, rank: int):
+        if len(unique_id) != 128:
+            raise InvalidArgument("nccl: the unique id is 128 bytes")
+        h = C.c_void_p()
+        _check(load_library().st_nccl_comm_init(unique_id, int(n_ranks), int(rank), C.byref(h)))
+        self.handle, self.n_ranks, self.rank = h.value, n_ranks, rank
+
+    def close(self):
+        if self.handle:
+            load_library().st_nccl_comm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def treecode_velocity_nccl(position_ptr: int, force_ptr: Optional[int], dipole_ptr: Optional[int],
+                           normal_ptr: Optional[int], n: int, params: TreecodeParams, u_out_ptr: int,
+                           comm: NcclComm, targets_ptr: Optional[int] = None, n_targets: int = 0,
+                           stream: int = 0) -> VelocityResult:
+    """One rank's call of the multi-GPU treecode with NCCL inside the library
+    (st_treecode_velocity_nccl): every rank holds all inputs on its device; u_out receives
+    every target's velocity (original order) on every rank; stats are the whole job's."""
+    L = load_library()
+    cp = _Particles(n, position_ptr, force_ptr, dipole_ptr, normal_ptr)
+    prm = params._c()
+    st = _Stats()
+    _check(L.st_treecode_velocity_nccl(C.byref(cp), targets_ptr, n_targets, C.byref(prm), u_out_ptr, comm.handle,
+                                       stream, C.byref(st)))
+    return _result(None, st)
 
 
 def ipc_export(device_ptr: int):

@@ -17,6 +17,7 @@
 
 #include "moments.cuh"
 #include "staging.cuh"
+#include "nccl_comm.cuh"
 #include "traverse.cuh"
 #include "tree.cuh"
 
@@ -1320,6 +1321,89 @@ st_status st_treecode_velocity_device_ev2(const st_particles* src, const double*
         run_treecode(d, targets, targets ? n_targets : src->n, *params, u_out, nullptr, shard, n_shards, s, ro,
                      false, nullptr, static_cast<cudaEvent_t>(weights_ready), nullptr,
                      static_cast<cudaEvent_t>(targets_ready));
+        raise_flags(ro);
+        fill_stats(stats, ro);
+        if (stats) stats->gpu_launches = g_launches;
+    });
+}
+
+}  // extern "C"
+
+struct st_comm {
+    NcclComm* c = nullptr;
+};
+
+extern "C" {
+
+st_status st_nccl_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        if (!id) fail(ST_INVALID_ARGUMENT, "nccl: null id");
+        nccl_unique_id(id);
+    });
+}
+
+st_status st_nccl_comm_init(const unsigned char id[128], int n_ranks, int rank, st_comm** comm) {
+    return guarded([&] {
+        if (!id || !comm) fail(ST_INVALID_ARGUMENT, "nccl: null argument");
+        ensure_device();
+        st_comm* c = new st_comm;
+        try {
+            c->c = nccl_comm_init(id, n_ranks, rank);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *comm = c;
+    });
+}
+
+void st_nccl_comm_free(st_comm* comm) {
+    if (!comm) return;
+    nccl_comm_free(comm->c);
+    delete comm;
+}
+
+st_status st_treecode_velocity_nccl(const st_particles* src, const double* targets, size_t n_targets,
+                                    const st_params* params, double* u_out, const st_comm* comm, void* stream,
+                                    st_stats* stats) {
+    return guarded([&] {
+        g_launches = 0;
+        validate_params(params);
+        if (!comm || !comm->c) fail(ST_INVALID_ARGUMENT, "nccl: null communicator");
+        const bool sto = params->stokeslet != 0, str = params->stresslet != 0;
+        validate_shape(src, sto, str);
+        if (targets && n_targets == 0) fail(ST_INVALID_ARGUMENT, "targets: empty target set");
+        ensure_device();
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const int rank = nccl_rank(comm->c), world = nccl_ranks(comm->c);
+        const size_t nt = targets ? n_targets : src->n;
+        DevParticles d;
+        d.n = src->n;
+        d.pos = src->position;
+        d.f = sto ? src->force_weight : nullptr;
+        d.h = str ? src->dipole_weight : nullptr;
+        d.nu = str ? src->normal : nullptr;
+        ST_CUDA(cudaMemsetAsync(u_out, 0, 3 * nt * sizeof(double), s));
+        SplitExchange x;
+        x.fn = nccl_exchange;
+        x.ctx = comm->c;
+        RunOut ro;
+        run_treecode(d, targets, nt, *params, u_out, nullptr, rank, world, s, ro, false, nullptr, nullptr,
+                     world > 1 ? &x : nullptr);
+        // the gather before any error is raised: a domain error is found by the rank whose
+        // shard holds the coincident pair, and every rank must take part in the collective
+        // counters: the three statistics, then how many ranks saw each error bit
+        unsigned long long* h = static_cast<unsigned long long*>(pinned_stage(5 * sizeof(unsigned long long)));
+        for (int k = 0; k < 3; ++k) h[k] = ro.stats[k];
+        h[3] = (unsigned long long)(ro.domain_err & 1);
+        h[4] = (unsigned long long)((ro.domain_err >> 1) & 1);
+        DevArray<unsigned long long> dst(5, s);
+        ST_CUDA(cudaMemcpyAsync(dst.get(), h, 5 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+        nccl_gather(comm->c, u_out, 3 * nt, dst.get(), 5, s);
+        ST_CUDA(cudaMemcpyAsync(h, dst.get(), 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        for (int k = 0; k < 3; ++k) ro.stats[k] = h[k];
+        ro.domain_err = (h[3] ? 1 : 0) | (h[4] ? 2 : 0);
         raise_flags(ro);
         fill_stats(stats, ro);
         if (stats) stats->gpu_launches = g_launches;

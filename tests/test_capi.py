@@ -167,3 +167,11 @@ def test_bench_far_flop_conventions():
     # executed flops at P = 10 (p = 8 with stresslets), as counted in the SASS
     assert bench.far_executed_flops(10) == 1226
     assert bench.f_far(8) / bench.far_executed_flops(10) == pytest.approx(27.9, abs=0.05)
+
+
+def test_nccl_unique_id_without_a_gpu():
+    """NCCL inside the library is loaded at first use (dlopen): the id of a new communicator
+    can be made on a host without a GPU."""
+    import paper_1811_12498_b200 as S
+    a, b = S.nccl_unique_id(), S.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
