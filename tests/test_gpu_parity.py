@@ -278,6 +278,19 @@ def test_treecode_cfg0_parity(S, need_ref, order, theta, n0):
     assert S.relative_error(u_ref, res.velocity) <= REL_TOL
 
 
+@pytest.mark.parametrize("order,sel", [(12, "both"), (14, "stokeslet_only"), (16, "both"), (16, "stresslet_only")])
+def test_treecode_high_orders(S, need_ref, order, sel):
+    """The top of the order range (kMaxOrder = 16, engine.hpp:23): far kernels up to
+    P = 18, where the harmonic recurrence's registers spill; still within 1e-12 of the
+    reference, interaction lists bit-exact."""
+    k = getattr(S.KernelSelection, sel)()
+    ps = S.generate("cube", 6000, 4242, True)
+    res, u_ref, pt_ref, st_ref = run_pair(S, need_ref, ps, order, 0.5, 250, sel=k)
+    assert np.array_equal(res.per_target, pt_ref)
+    assert res.stats.farfield_evals == st_ref["farfield_evals"]
+    assert S.relative_error(u_ref, res.velocity) <= REL_TOL
+
+
 def test_treecode_error_vs_direct_matches_reference(S, need_ref):
     ps = S.generate("cube", 10000, 12345, True)
     res, u_ref, _, _ = run_pair(S, need_ref, ps, 6, 0.5, 500)
