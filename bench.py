@@ -799,7 +799,12 @@ def measure_moments(S, step, cfg, ps, peak, world):
                     "reference_equivalent_frac": f_ref / t * 1e-12 / peak,
                     "leaf_algorithmic_tflops": f_leaf / t * 1e-12,
                     "leaf_algorithmic_frac": f_leaf / t * 1e-12 / peak,
-                    "bound": "max(bytes / HBM, flops / FP64): FP64 (>= 40 flop/B, SURVEY.md 8d)"})
+                    "bound": "max(bytes / HBM, flops / FP64): FP64 (>= 40 flop/B, SURVEY.md 8d)",
+                    "binding_resource": "k_moments (leaf sums, most of the pass): the shared-memory pipe, 82% of "
+                                        "its wavefront capacity at cfg4 (ncu: six broadcast LDS.128 of weights and "
+                                        "six per-lane power loads per particle and warp for 24 FMAs per thread); "
+                                        "k_fold: issue-bound on index arithmetic (FP64 7%); top M2M levels: "
+                                        "latency-bound, ~73 us each (profiles/r02_moments_ncu.md, DESIGN.md sec. 9)"})
     return out
 
 
